@@ -1,0 +1,123 @@
+/*
+ * bri_b200.h — C ABI of the B200 BRI hot path (libbri_b200.so).
+ *
+ * The reference (`bri`, pure Python) has no FFI of its own: its hot path calls
+ * numpy/scipy, i.e. OpenBLAS dgemm and LAPACK dgetrf/dgetrs, from
+ *   pkg/src/bri/core.py:173-181   multiply      (x @ y)
+ *   pkg/src/bri/core.py:184-197   subtract      (x -= y)
+ *   pkg/src/bri/core.py:238-263   invert_dense  (dgetrf on x.T, pivot test, dgetrs vs I)
+ *   pkg/src/bri/core.py:212-235   lu_factor     (dgetrf on x)
+ *   pkg/src/bri/engine.py:157-180 _fold         (r - l @ (inv(p) @ rt) per Schur node)
+ * The entry points below are what a maintainer binds in place of those calls
+ * (ctypes stub in INTEGRATION.md).  Plain pointers and sizes only; all buffers
+ * are caller-owned device memory; nothing throws across the ABI.
+ *
+ * Memory model: an *arena* is caller-owned device memory holding `nslots`
+ * blocks of order n, slot s at base + s * n * ld doubles, each block stored
+ * row-major with row stride ld (ld % 8 == 0, ld >= n) — i.e. exactly the bytes
+ * of the reference's C-ordered (b, b) float64 ndarray.  Kernels read a slot as
+ * the column-major transpose (the LAPACK view the reference factors,
+ * core.py:249).  Items name slots by index.
+ *
+ * Return value: 0 on success, < 0 on a CUDA / argument error
+ * (bri_last_error() has the message).  Singular pivots are NOT errors at this
+ * level: they are reported per item in `status` (0 = ok, otherwise the 1-based
+ * index of the first pivot with |u_ii| <= n * eps * max|A|, NaN flagged), the
+ * caller maps them to SingularBlockError / SingularPivotError
+ * (errors.py:26-69) as the reference does.
+ */
+#ifndef BRI_B200_H
+#define BRI_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bri_ctx bri_ctx;
+typedef struct bri_arena bri_arena;
+
+/* ABI version (major * 100 + minor). */
+int bri_version(void);
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* bri_last_error(void);
+
+/* Per-device context: kernel attributes, staging buffers, TMA encoder. */
+int bri_ctx_create(int device, bri_ctx** out);
+void bri_ctx_destroy(bri_ctx* ctx);
+
+/* Wrap caller-owned device memory as an arena (builds the TMA descriptors). */
+int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_arena** out);
+void bri_arena_destroy(bri_arena* arena);
+
+/*
+ * Schur nodes, batched — replaces engine.py:157-180 (_fold) for `count` nodes.
+ * items: 7 ints per node: slots (p, rt, l, r, out, f, w); f and w are scratch
+ * slots (f receives the LU factors of p, w the solve).  Computes, per node,
+ *     out = r - l @ inv(p) @ rt          (row-major block semantics)
+ * with 1 factorization + 1 solve + 1 fused GEMM-subtract.  p/rt/l/r are not
+ * modified (out may alias r).  status (device, count ints): pivot test of p.
+ */
+int bri_schur_batch(bri_arena* arena, void* stream, int count, const int* items, int* status);
+
+/*
+ * Block inverses, batched — replaces core.py:238-263 (invert_dense).
+ * items: 3 ints per block: slots (in, f, out); f is scratch; in is not modified.
+ * status (device, count ints): pivot test of in.
+ */
+int bri_invert_batch(bri_arena* arena, void* stream, int count, const int* items, int* status);
+
+/*
+ * LU with partial pivoting in place, batched — dgetrf semantics on the
+ * column-major view of each slot (i.e. on the transpose of the row-major
+ * block, as core.py:249).  perm (device, count * n ints, may be NULL):
+ * 0-based row permutation, (P X)[x] = X[perm[x]].  ipiv (device, count * n,
+ * may be NULL): LAPACK-style 0-based interchanges.  status as above.
+ */
+int bri_getrf_batch(bri_arena* arena, void* stream, int count, const int* slots, int* ipiv,
+                    int* perm, int* status);
+
+/*
+ * Solve with LU factors, batched — dgetrs(trans = 'N') semantics on the
+ * column-major views (core.py:259): dst = X^-1 * src where X's factors are in
+ * slot f (from bri_getrf_batch) and perm its row permutation (device, count * n).
+ * items: 3 ints (f, src, dst), dst != src.
+ */
+int bri_getrs_batch(bri_arena* arena, void* stream, int count, const int* items, const int* perm);
+
+/*
+ * GEMM, batched — replaces core.py:173-181 (multiply) fused with
+ * core.py:184-197 (subtract).  Column-major window semantics on each slot:
+ *   C_out[c_r0:+M, c_c0:+N] = beta * C_in[...] + alpha * A[a_r0:+M, a_c0:+K] * B[b_r0:+K, b_c0:+N]
+ * items: 4 ints per product: slots (A, B, C_in, C_out).  For row-major blocks
+ * x @ y pass A = y, B = x.  beta == 0 never reads C_in.
+ */
+int bri_gemm(bri_arena* arena, void* stream, int count, const int* items, int M, int N, int K,
+             int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha,
+             double beta);
+
+/* out = alpha * x + beta * y elementwise over whole slots; items: (x, y, out). */
+int bri_axpby(bri_arena* arena, void* stream, int count, const int* items, double alpha,
+              double beta);
+
+/* out = transpose(src) over whole slots; items: (src, out), out != src. */
+int bri_transpose(bri_arena* arena, void* stream, int count, const int* items);
+
+/*
+ * Block gather — replaces the per-fetch copy of providers.py:318-336 +
+ * core.py:92-98 for a matrix resident in device memory.  M: dense row-major
+ * device matrix with leading dim ldm (elements); items: 3 ints per block
+ * (block row i, block col j, destination slot), 0-based, block order = arena n.
+ */
+int bri_gather_blocks(bri_arena* arena, void* stream, const double* M, long long ldm, int count,
+                      const int* items);
+
+/* FP64 DMMA throughput probe (register-only mma.sync loop on every SM);
+ * writes achieved TFLOP/s.  Used by bench.py as the roofline denominator. */
+int bri_fp64_peak(void* stream, int iters, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BRI_B200_H */

@@ -1,0 +1,72 @@
+// Internal (C++) interfaces between the kernel files and the C-ABI layer.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace bri {
+
+constexpr int NBMAX = 32;        // LU panel width upper bound
+constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
+
+// Arena geometry: nslots column-major n x n blocks (X-world), leading dim ld
+// (multiple of 8, >= n), slot i at base + i * slot_elems.
+struct ArenaView {
+  double* base;
+  int n;
+  int ld;
+  long long slot_elems;
+  int nslots;
+};
+
+struct GemmParams {
+  double* base;
+  int ld;
+  long long slot_elems;
+  const int* items;  // device: 4 ints per item (slot A, slot B, slot C_in, slot C_out)
+  int M, N, K;
+  int a_r0, a_c0, b_r0, b_c0, c_r0, c_c0;
+  double alpha, beta;
+  int tiles_m, tiles_n;
+};
+
+int gemm_smem_bytes();
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p,
+                        int count, cudaStream_t stream);
+cudaError_t launch_scale_copy(const GemmParams& p, int count, cudaStream_t stream);
+
+// ---------------------------------------------------------------- LU pieces
+struct LuScratch {
+  // device arrays, per item
+  int* ipiv;      // n
+  int* pi;        // n   (row permutation: (P X)[x] = X[pi[x]])
+  int* sigma;     // n   (per panel: source row of each segment position)
+  int* pairs;     // npanels * (1 + 2 * NBMAX)
+  unsigned long long* scale_bits;  // 1 (max |X| as double bits)
+  int* status;    // 1
+};
+
+cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
+                          unsigned long long* scale_bits, cudaStream_t s);
+cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStream_t s);
+cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, const int* pi,
+                            int pi_stride, bool identity_src, cudaStream_t s);
+cudaError_t launch_pi_init(int* pi, int n, int count, cudaStream_t s);
+int panel_width(int n);
+cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
+                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
+cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
+                            const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
+cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
+                              const unsigned long long* scale_bits, int* status, cudaStream_t s);
+cudaError_t launch_trsm_leaf(const ArenaView& a, const int* fw_slots, int count, bool lower,
+                             int r0, int nr, int nrhs, cudaStream_t s);
+
+// Fused one-CTA node / inverse for n <= SMALL_MAX.
+// items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.
+cudaError_t launch_small_node(const ArenaView& a, const int* items, int count, int mode,
+                              int* status, cudaStream_t s);
+
+}  // namespace bri

@@ -1,0 +1,559 @@
+// C ABI of libbri_b200.so (include/bri_b200.h): contexts, arenas (TMA
+// descriptors over caller-owned device memory) and the batched hot-path
+// operations that stand in for the reference's BLAS/LAPACK calls.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bri_b200.h"
+#include "bri_common.cuh"
+#include "bri_internal.h"
+
+using namespace bri;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const char* what, cudaError_t e) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return -1;
+}
+
+int fail_msg(const std::string& msg) {
+  g_last_error = msg;
+  return -2;
+}
+
+#define BRI_CHECK(call)                          \
+  do {                                           \
+    cudaError_t _e = (call);                     \
+    if (_e != cudaSuccess) return fail(#call, _e); \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// Grow-only device buffer whose reuse is ordered by the (single) stream a
+// context is driven from.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need, cudaStream_t s) {
+    if (need <= bytes) return 0;
+    size_t nb = need + need / 2 + 4096;
+    if (ptr != nullptr) BRI_CHECK(cudaFreeAsync(ptr, s));
+    ptr = nullptr;
+    BRI_CHECK(cudaMallocAsync(&ptr, nb, s));
+    bytes = nb;
+    return 0;
+  }
+};
+
+}  // namespace
+
+struct bri_ctx {
+  int device = 0;
+  DevBuf items;   // uploaded item arrays
+  DevBuf lu;      // LU scratch
+  std::vector<int> host;  // staging for item arrays
+};
+
+struct bri_arena {
+  bri_ctx* ctx = nullptr;
+  ArenaView v{};
+  alignas(64) CUtensorMap tmA;
+  alignas(64) CUtensorMap tmB;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+// Upload `words` host ints into the context's device buffer (stream-ordered).
+int upload(bri_ctx* ctx, cudaStream_t s, const std::vector<int>& h, int** dev) {
+  const size_t bytes = h.size() * sizeof(int);
+  if (int rc = ctx->items.ensure(bytes, s)) return rc;
+  BRI_CHECK(cudaMemcpyAsync(ctx->items.ptr, h.data(), bytes, cudaMemcpyHostToDevice, s));
+  *dev = static_cast<int*>(ctx->items.ptr);
+  return 0;
+}
+
+struct LuLayout {
+  int n, count, npanels, pair_stride;
+  size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, total;
+};
+
+LuLayout lu_layout(int n, int count) {
+  LuLayout L;
+  L.n = n;
+  L.count = count;
+  const int nb = panel_width(n);
+  L.npanels = (n + nb - 1) / nb;
+  L.pair_stride = L.npanels * (1 + 2 * NBMAX);
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    size_t o = off;
+    off += (b + 255) & ~size_t(255);
+    return o;
+  };
+  L.off_ipiv = take((size_t)count * n * 4);
+  L.off_pi = take((size_t)count * n * 4);
+  L.off_sigma = take((size_t)count * n * 4);
+  L.off_pairs = take((size_t)count * L.pair_stride * 4);
+  L.off_scale = take((size_t)count * 8);
+  L.off_status = take((size_t)count * 4);
+  L.total = off;
+  return L;
+}
+
+LuScratch lu_scratch(void* base, const LuLayout& L) {
+  char* b = static_cast<char*>(base);
+  LuScratch s;
+  s.ipiv = reinterpret_cast<int*>(b + L.off_ipiv);
+  s.pi = reinterpret_cast<int*>(b + L.off_pi);
+  s.sigma = reinterpret_cast<int*>(b + L.off_sigma);
+  s.pairs = reinterpret_cast<int*>(b + L.off_pairs);
+  s.scale_bits = reinterpret_cast<unsigned long long*>(b + L.off_scale);
+  s.status = reinterpret_cast<int*>(b + L.off_status);
+  return s;
+}
+
+int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, int M, int N, int K,
+              int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta) {
+  GemmParams p{};
+  p.base = ar->v.base;
+  p.ld = ar->v.ld;
+  p.slot_elems = ar->v.slot_elems;
+  p.items = dev_items;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.a_r0 = a_r0;
+  p.a_c0 = a_c0;
+  p.b_r0 = b_r0;
+  p.b_c0 = b_c0;
+  p.c_r0 = c_r0;
+  p.c_c0 = c_c0;
+  p.alpha = alpha;
+  p.beta = beta;
+  BRI_CHECK(launch_gemm(ar->tmA, ar->tmB, p, count, s));
+  return 0;
+}
+
+// Blocked right-looking LU (dgetrf) of `count` slots in place.
+// gemm_items: device array of 4*count ints (F, F, F, F) per item.
+int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, int count,
+                 const LuLayout& L, const LuScratch& sc) {
+  const ArenaView& v = ar->v;
+  const int n = v.n;
+  BRI_CHECK(cudaMemsetAsync(sc.scale_bits, 0, (size_t)count * 8, s));
+  BRI_CHECK(cudaMemsetAsync(sc.pairs, 0, (size_t)count * L.pair_stride * 4, s));
+  BRI_CHECK(launch_pi_init(sc.pi, n, count, s));
+  BRI_CHECK(launch_maxabs(v, dev_slots, count, sc.scale_bits, s));
+  const int nb = panel_width(n);
+  for (int j0 = 0, pidx = 0; j0 < n; j0 += nb, ++pidx) {
+    const int w = (n - j0) < nb ? (n - j0) : nb;
+    BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
+    BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
+    const int rest = n - j0 - w;
+    if (rest > 0) {
+      if (int rc = gemm_call(ar, s, dev_ffff, count, rest, rest, w, j0 + w, j0, j0, j0 + w, j0 + w,
+                             j0 + w, -1.0, 1.0))
+        return rc;
+    }
+  }
+  BRI_CHECK(launch_diag_check(v, dev_slots, count, sc.scale_bits, sc.status, s));
+  return 0;
+}
+
+// Recursive triangular solve on W with the factor F (both from the item list).
+// fw: device (F, W) pairs; gemm_fw: device (F, W, W, W) quads.
+int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, int count, bool lower,
+             int r0, int nr, int nrhs) {
+  if (nr <= NBMAX) {
+    BRI_CHECK(launch_trsm_leaf(ar->v, fw, count, lower, r0, nr, nrhs, s));
+    return 0;
+  }
+  int h = ((nr / 2) + NBMAX - 1) / NBMAX * NBMAX;
+  if (h >= nr) h = nr - NBMAX;
+  if (lower) {
+    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs)) return rc;
+    // W[r0+h : r0+nr, :] -= L[r0+h : r0+nr, r0 : r0+h] * W[r0 : r0+h, :]
+    if (int rc = gemm_call(ar, s, gemm_fw, count, nr - h, nrhs, h, r0 + h, r0, r0, 0, r0 + h, 0, -1.0, 1.0))
+      return rc;
+    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs);
+  }
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs)) return rc;
+  // W[r0 : r0+h, :] -= U[r0 : r0+h, r0+h : r0+nr] * W[r0+h : r0+nr, :]
+  if (int rc = gemm_call(ar, s, gemm_fw, count, h, nrhs, nr - h, r0, r0 + h, r0 + h, 0, r0, 0, -1.0, 1.0))
+    return rc;
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs);
+}
+
+// ---------------------------------------------------------------- misc kernels
+__global__ void axpby_kernel(ArenaView a, const int* items, double alpha, double beta) {
+  const int* it = items + 3 * blockIdx.y;
+  const double* x = a.base + (long long)it[0] * a.slot_elems;
+  const double* y = a.base + (long long)it[1] * a.slot_elems;
+  double* o = a.base + (long long)it[2] * a.slot_elems;
+  for (int j = blockIdx.x; j < a.n; j += gridDim.x)
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+      const long long off = i + (long long)j * a.ld;
+      o[off] = alpha * x[off] + beta * y[off];
+    }
+}
+
+__global__ void transpose_kernel(ArenaView a, const int* items) {
+  __shared__ double tile[32][33];
+  const int* it = items + 2 * blockIdx.z;
+  const double* src = a.base + (long long)it[0] * a.slot_elems;
+  double* dst = a.base + (long long)it[1] * a.slot_elems;
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + threadIdx.x, j = j0 + r;
+    if (i < a.n && j < a.n) tile[r][threadIdx.x] = src[i + (long long)j * a.ld];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = j0 + threadIdx.x, j = i0 + r;
+    if (i < a.n && j < a.n) dst[i + (long long)j * a.ld] = tile[threadIdx.x][r];
+  }
+}
+
+// Copy row-major blocks M[i*n : (i+1)*n, j*n : (j+1)*n] of a dense row-major
+// matrix (leading dim ldm) into arena slots.  items: (block row i, block col j,
+// slot), 0-based.  Arena slots hold the row-major block bytes (ld stride).
+__global__ void gather_kernel(ArenaView a, const double* M, long long ldm, const int* items) {
+  const int* it = items + 3 * blockIdx.y;
+  const long long r0 = (long long)it[0] * a.n, c0 = (long long)it[1] * a.n;
+  double* dst = a.base + (long long)it[2] * a.slot_elems;
+  for (int r = blockIdx.x; r < a.n; r += gridDim.x) {
+    const double* src = M + (r0 + r) * ldm + c0;
+    double* d = dst + (long long)r * a.ld;
+    for (int c = threadIdx.x; c < a.n; c += blockDim.x) d[c] = src[c];
+  }
+}
+
+__global__ void fp64_peak_kernel(double* sink, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_8x8x4(c[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1234.5678) sink[0] = s;
+}
+
+}  // namespace
+
+// ==================================================================== C ABI
+extern "C" {
+
+int bri_version(void) { return 100; }
+
+const char* bri_last_error(void) { return g_last_error.c_str(); }
+
+int bri_ctx_create(int device, bri_ctx** out) {
+  if (out == nullptr) return fail_msg("bri_ctx_create: null out");
+  BRI_CHECK(cudaSetDevice(device));
+  if (get_encoder() == nullptr) return fail_msg("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  bri_ctx* c = new bri_ctx();
+  c->device = device;
+  *out = c;
+  return 0;
+}
+
+void bri_ctx_destroy(bri_ctx* ctx) {
+  if (ctx == nullptr) return;
+  cudaDeviceSynchronize();
+  if (ctx->items.ptr) cudaFree(ctx->items.ptr);
+  if (ctx->lu.ptr) cudaFree(ctx->lu.ptr);
+  delete ctx;
+}
+
+int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_arena** out) {
+  if (ctx == nullptr || base == nullptr || out == nullptr) return fail_msg("bri_arena_create: null argument");
+  if (n < 1 || ld < n || (ld % 8) != 0 || nslots < 1)
+    return fail_msg("bri_arena_create: need n >= 1, ld >= n, ld % 8 == 0, nslots >= 1");
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail_msg("bri_arena_create: base not 16-byte aligned");
+  bri_arena* a = new bri_arena();
+  a->ctx = ctx;
+  a->v.base = base;
+  a->v.n = n;
+  a->v.ld = ld;
+  a->v.slot_elems = (long long)n * ld;
+  a->v.nslots = nslots;
+  EncodeTiledFn enc = get_encoder();
+  const cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)n, (cuuint64_t)nslots};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)a->v.slot_elems * 8};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const cuuint32_t boxA[3] = {8, 16, 1};
+  const cuuint32_t boxB[3] = {16, 128, 1};
+  CUresult r1 = enc(&a->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxA, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r2 = enc(&a->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+    delete a;
+    return fail_msg("cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" + std::to_string((int)r2));
+  }
+  *out = a;
+  return 0;
+}
+
+void bri_arena_destroy(bri_arena* arena) { delete arena; }
+
+int bri_gemm(bri_arena* ar, void* stream, int count, const int* items, int M, int N, int K, int a_r0,
+             int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta) {
+  if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_gemm: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 4 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  return gemm_call(ar, s, dev, count, M, N, K, a_r0, a_c0, b_r0, b_c0, c_r0, c_c0, alpha, beta);
+}
+
+int bri_axpby(bri_arena* ar, void* stream, int count, const int* items, double alpha, double beta) {
+  if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_axpby: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 3 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int gx = ar->v.n < 512 ? ar->v.n : 512;
+  axpby_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, dev, alpha, beta);
+  BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_transpose(bri_arena* ar, void* stream, int count, const int* items) {
+  if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_transpose: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 2 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int t = (ar->v.n + 31) / 32;
+  transpose_kernel<<<dim3(t, t, count), dim3(32, 8), 0, s>>>(ar->v, dev);
+  BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, int* ipiv, int* perm,
+                    int* status) {
+  if (ar == nullptr || slots == nullptr || count < 0) return fail_msg("bri_getrf_batch: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  std::vector<int> h(5 * (size_t)count);
+  for (int i = 0; i < count; ++i) {
+    h[i] = slots[i];
+    for (int q = 0; q < 4; ++q) h[count + 4 * i + q] = slots[i];
+  }
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  LuLayout L = lu_layout(n, count);
+  if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
+  LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  if (int rc = getrf_device(ar, s, dev, dev + count, count, L, sc)) return rc;
+  if (ipiv) BRI_CHECK(cudaMemcpyAsync(ipiv, sc.ipiv, (size_t)count * n * 4, cudaMemcpyDeviceToDevice, s));
+  if (perm) BRI_CHECK(cudaMemcpyAsync(perm, sc.pi, (size_t)count * n * 4, cudaMemcpyDeviceToDevice, s));
+  if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, const int* perm) {
+  if (ar == nullptr || items == nullptr || perm == nullptr || count < 0)
+    return fail_msg("bri_getrs_batch: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  // layout: [(src,dst) | (F,dst) | (F,dst,dst,dst)]
+  std::vector<int> h;
+  h.reserve(8 * (size_t)count);
+  for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 1]); h.push_back(items[3 * i + 2]); }
+  for (int i = 0; i < count; ++i) { h.push_back(items[3 * i]); h.push_back(items[3 * i + 2]); }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(items[3 * i]);
+    for (int q = 0; q < 3; ++q) h.push_back(items[3 * i + 2]);
+  }
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  BRI_CHECK(launch_permcopy(ar->v, dev, count, perm, n, false, s));
+  if (int rc = trsm_rec(ar, s, dev + 2 * count, dev + 4 * count, count, true, 0, n, n)) return rc;
+  return trsm_rec(ar, s, dev + 2 * count, dev + 4 * count, count, false, 0, n, n);
+}
+
+int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
+  if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_invert_batch: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  if (n <= SMALL_MAX) {
+    std::vector<int> h(5 * (size_t)count);
+    for (int i = 0; i < count; ++i) {
+      h[5 * i + 0] = items[3 * i];
+      h[5 * i + 1] = items[3 * i];
+      h[5 * i + 2] = items[3 * i];
+      h[5 * i + 3] = items[3 * i];
+      h[5 * i + 4] = items[3 * i + 2];
+    }
+    int* dev = nullptr;
+    if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+    BRI_CHECK(launch_small_node(ar->v, dev, count, 1, status, s));
+    return 0;
+  }
+  // layout: [F slots | (in,F) pairs | (F,F,F,F) | (F,out) | (F,out,out,out)]
+  std::vector<int> h;
+  h.reserve(13 * (size_t)count);
+  for (int i = 0; i < count; ++i) h.push_back(items[3 * i + 1]);
+  for (int i = 0; i < count; ++i) { h.push_back(items[3 * i]); h.push_back(items[3 * i + 1]); }
+  for (int i = 0; i < count; ++i) for (int q = 0; q < 4; ++q) h.push_back(items[3 * i + 1]);
+  for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 1]); h.push_back(items[3 * i + 2]); }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(items[3 * i + 1]);
+    for (int q = 0; q < 3; ++q) h.push_back(items[3 * i + 2]);
+  }
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_f = dev;
+  const int* d_inf = dev + count;
+  const int* d_ffff = dev + 3 * count;
+  const int* d_fo = dev + 7 * count;
+  const int* d_fooo = dev + 9 * count;
+  LuLayout L = lu_layout(n, count);
+  if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
+  LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  BRI_CHECK(launch_copy(ar->v, d_inf, count, s));
+  if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
+  // out = P * I, then L and U solves in place (dgetrs against the identity)
+  BRI_CHECK(launch_permcopy(ar->v, d_fo, count, sc.pi, n, true, s));
+  if (int rc = trsm_rec(ar, s, d_fo, d_fooo, count, true, 0, n, n)) return rc;
+  if (int rc = trsm_rec(ar, s, d_fo, d_fooo, count, false, 0, n, n)) return rc;
+  if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
+  if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_schur_batch: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  auto I = [&](int i, int k) { return items[7 * i + k]; };  // p, rt, l, r, out, f, w
+  if (n <= SMALL_MAX) {
+    std::vector<int> h(5 * (size_t)count);
+    for (int i = 0; i < count; ++i)
+      for (int k = 0; k < 5; ++k) h[5 * i + k] = I(i, k);
+    int* dev = nullptr;
+    if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+    BRI_CHECK(launch_small_node(ar->v, dev, count, 0, status, s));
+    return 0;
+  }
+  // layout: [F | (p,F) | (F,F,F,F) | (l,W) | (F,W) | (F,W,W,W) | (rt,W,r,out)]
+  std::vector<int> h;
+  h.reserve(17 * (size_t)count);
+  for (int i = 0; i < count; ++i) h.push_back(I(i, 5));
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 0)); h.push_back(I(i, 5)); }
+  for (int i = 0; i < count; ++i) for (int q = 0; q < 4; ++q) h.push_back(I(i, 5));
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 2)); h.push_back(I(i, 6)); }
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 5)); h.push_back(I(i, 6)); }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(I(i, 5));
+    for (int q = 0; q < 3; ++q) h.push_back(I(i, 6));
+  }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(I(i, 1));
+    h.push_back(I(i, 6));
+    h.push_back(I(i, 3));
+    h.push_back(I(i, 4));
+  }
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_f = dev;
+  const int* d_pf = dev + count;
+  const int* d_ffff = dev + 3 * count;
+  const int* d_lw = dev + 7 * count;
+  const int* d_fw = dev + 9 * count;
+  const int* d_fwww = dev + 11 * count;
+  const int* d_final = dev + 15 * count;
+  LuLayout L = lu_layout(n, count);
+  if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
+  LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
+  if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
+  // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
+  BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
+  if (int rc = trsm_rec(ar, s, d_fw, d_fwww, count, true, 0, n, n)) return rc;
+  if (int rc = trsm_rec(ar, s, d_fw, d_fwww, count, false, 0, n, n)) return rc;
+  if (int rc = gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0)) return rc;
+  if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ldm, int count,
+                      const int* items) {
+  if (ar == nullptr || M == nullptr || items == nullptr || count < 0) return fail_msg("bri_gather_blocks: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 3 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int gx = ar->v.n < 1024 ? ar->v.n : 1024;
+  gather_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, dev);
+  BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_fp64_peak(void* stream, int iters, double* tflops) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev = 0, sms = 0;
+  BRI_CHECK(cudaGetDevice(&dev));
+  BRI_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* sink = nullptr;
+  BRI_CHECK(cudaMallocAsync(&sink, 8, s));
+  const int blocks = sms * 2, threads = 256;
+  cudaEvent_t e0, e1;
+  BRI_CHECK(cudaEventCreate(&e0));
+  BRI_CHECK(cudaEventCreate(&e1));
+  fp64_peak_kernel<<<blocks, threads, 0, s>>>(sink, iters / 4);
+  BRI_CHECK(cudaEventRecord(e0, s));
+  fp64_peak_kernel<<<blocks, threads, 0, s>>>(sink, iters);
+  BRI_CHECK(cudaEventRecord(e1, s));
+  BRI_CHECK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  BRI_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  BRI_CHECK(cudaFreeAsync(sink, s));
+  const double flops = (double)blocks * (threads / 32) * iters * 8 * (2.0 * 8 * 8 * 4);
+  if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+"""Host scheduler: the BRI recursion as a deduplicated, level-ordered DAG.
+
+Reference semantics (engine.py:196-241): a node's value depends only on its
+frame's *base* block indices (after the target's view permutation,
+providers.py:123-145) and on its label when n > 2 (a leaf always eliminates
+D).  The reference walks the literal tree and refetches shared subtrees by
+design (engine.py:26-27); the scheduler here evaluates every
+distinct (base rows, base cols, label|None) key once, across all requested
+targets.  Each node is computed by the same device kernels on the same
+operand bytes whichever schedule reaches it, so the deduplicated schedule
+is bit-identical to the tree walk (checked in tests/test_gpu_engine.py).
+
+Frames of order n only consume frames of order n-1, so the DAG is executed
+level by level (n = 2 .. k) with all nodes of a level batched into the same
+kernel launches; level n-1 values are dropped once level n is done.
+
+Errors are mapped back to the reference's report: `first_failure` replays
+the reference's depth-first evaluation order (pivot subtree, pivot
+inversion, then rt / l / r subtrees; engine.py:157-180) over the per-node
+pivot statuses and returns the first failing event, so the
+SingularPivotError path equals the one the reference raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .errors import SingularBlockError, SingularPivotError
+from .frames import PLAN, Frame, Quadrant, root_frame, split_frame
+
+__all__ = ["DagNode", "Schedule", "build_schedule", "build_from_specs", "target_maps"]
+
+
+@dataclass
+class DagNode:
+    nid: int
+    n: int                      # frame order (level)
+    key: tuple                  # (base rows, base cols, label | None)
+    operands: tuple             # 4 refs in role order (pivot, rt, l, r)
+    # a ref is ("m", i, j) for block M_ij of the base matrix, or ("v", nid)
+
+
+def target_maps(alpha: int, beta: int):
+    """Index maps of the view for target (alpha, beta): rows 1<->beta, cols 1<->alpha
+    (providers.py:123-145)."""
+
+    def mr(i):
+        return beta if i == 1 else (1 if i == beta else i)
+
+    def mc(j):
+        return alpha if j == 1 else (1 if j == alpha else j)
+
+    return mr, mc
+
+
+def _identity(i):
+    return i
+
+
+@dataclass
+class Schedule:
+    k: int
+    specs: list                                   # per root: (frame, row map, col map)
+    nodes: list = field(default_factory=list)
+    index: dict = field(default_factory=dict)
+    roots: list = field(default_factory=list)     # node id per root
+    paths0: list = field(default_factory=list)    # branch path of each root (root label first)
+
+    def key_of(self, frame: Frame, mr, mc) -> tuple:
+        return (tuple(mr(r) for r in frame.rows), tuple(mc(c) for c in frame.cols),
+                frame.label if frame.n > 2 else None)
+
+    def _visit(self, frame: Frame, mr, mc) -> int:
+        key = self.key_of(frame, mr, mc)
+        hit = self.index.get(key)
+        if hit is not None:
+            return hit
+        if frame.n == 2:
+            (r1, r2), (c1, c2) = frame.rows, frame.cols
+            spot = {Quadrant.A: (r1, c1), Quadrant.B: (r1, c2),
+                    Quadrant.C: (r2, c1), Quadrant.D: (r2, c2)}
+            ops = tuple(("m", mr(spot[q][0]), mc(spot[q][1])) for q in PLAN[Quadrant.D])
+        else:
+            kids = {ch.label: ch for ch in split_frame(frame)}
+            roles = PLAN[frame.label.mirror]
+            ops = tuple(("v", self._visit(kids[q], mr, mc)) for q in roles)
+        nid = len(self.nodes)
+        self.nodes.append(DagNode(nid, frame.n, key, ops))
+        self.index[key] = nid
+        return nid
+
+    # -------------------------------------------------------------- queries
+    def levels(self) -> dict:
+        out: dict = {}
+        for node in self.nodes:
+            out.setdefault(node.n, []).append(node.nid)
+        return dict(sorted(out.items()))
+
+    def tree_nodes(self, t: int) -> int:
+        """Nodes the reference's literal recursion visits for root t."""
+        n = self.specs[t][0].n
+        return (4 ** (n - 1) - 1) // 3
+
+    def m_blocks_used(self) -> set:
+        used = set()
+        for node in self.nodes:
+            for ref in node.operands:
+                if ref[0] == "m":
+                    used.add((ref[1], ref[2]))
+        return used
+
+    def peak_level_blocks(self) -> int:
+        """Live node values at the widest adjacent level pair (outputs only)."""
+        lv = self.levels()
+        ns = sorted(lv)
+        best = len(lv[ns[0]])
+        for a, b in zip(ns, ns[1:]):
+            best = max(best, len(lv[a]) + len(lv[b]))
+        return best
+
+    # ---------------------------------------------------- reference replay
+    def walk(self, t: int, on_event=None, on_node=None, skip: set | None = None, path0=None):
+        """Visit root t's tree in the reference's order (engine.py:157-180, 214-240).
+
+        on_event(nid, path, frame) fires at each pivot inversion, on_node(nid,
+        path, frame) after each node completes (the trace hook's moment).
+        Subtrees whose node id is in `skip` are not re-entered.
+        """
+        frame0, mr, mc = self.specs[t]
+
+        def rec(frame: Frame, path: tuple):
+            nid = self.index[self.key_of(frame, mr, mc)]
+            if skip is not None and nid in skip:
+                if on_node is not None:
+                    on_node(nid, path, frame)
+                return
+            if frame.n == 2:
+                if on_event is not None:
+                    on_event(nid, path, frame)
+            else:
+                kids = {ch.label: ch for ch in split_frame(frame)}
+                roles = PLAN[frame.label.mirror]
+                rec(kids[roles[0]], path + (roles[0],))
+                if on_event is not None:
+                    on_event(nid, path, frame)
+                for q in roles[1:]:
+                    rec(kids[q], path + (q,))
+            if skip is not None:
+                skip.add(nid)
+            if on_node is not None:
+                on_node(nid, path, frame)
+
+        rec(frame0, tuple(path0) if path0 is not None else self.paths0[t])
+
+    def first_failure(self, pivot_status, root_status, b: int):
+        """Raise the error the reference would raise first, if any.
+
+        pivot_status[nid] != 0: node nid's pivot inversion failed (1-based
+        pivot index); root_status[t] != 0: target t's final inversion failed
+        (None when the roots are not inverted, e.g. reduce_frame).
+        Targets are replayed in the order given (invert_full is row-major).
+        """
+        if root_status is None:
+            root_status = [0] * len(self.specs)
+        if not any(pivot_status) and not any(root_status):
+            return
+        clean: set = set()
+
+        def on_event(nid, path, frame):
+            if pivot_status[nid]:
+                raise SingularPivotError(path, frame.anchor)
+
+        for t in range(len(self.specs)):
+            self.walk(t, on_event=on_event, skip=clean)
+            if root_status[t]:
+                raise SingularBlockError(int(root_status[t]), b)
+
+
+def build_schedule(k: int, targets) -> Schedule:
+    """Deduplicated DAG over the union of the targets' reduction trees.
+
+    targets: (alpha, beta) pairs, 1-based, in the order results are wanted.
+    """
+    specs = [(root_frame(k),) + target_maps(a, b) for a, b in targets]
+    return build_from_specs(k, specs)
+
+
+def build_from_specs(k: int, specs, paths0=None) -> Schedule:
+    """DAG over arbitrary root frames with their (row, col) index maps."""
+    sched = Schedule(k=k, specs=list(specs))
+    sched.paths0 = [tuple(p) for p in paths0] if paths0 is not None else [(f.label,) for f, _, _ in specs]
+    for frame, mr, mc in sched.specs:
+        sched.roots.append(sched._visit(frame, mr or _identity, mc or _identity))
+    sched.specs = [(f, mr or _identity, mc or _identity) for f, mr, mc in sched.specs]
+    return sched

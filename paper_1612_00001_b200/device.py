@@ -1,0 +1,183 @@
+"""Device slot arena: the bounded-HBM block store behind every BRI run.
+
+An arena is one torch CUDA tensor of shape (nslots, n, ld) float64 — slot s
+holds one b x b block with exactly the bytes of the reference's C-ordered
+ndarray (row stride ld, ld a multiple of 8) — wrapped by a `bri_arena` handle
+that carries the TMA descriptors the kernels load through.  Slots are handed
+out by a free list and every allocation is reported to the workspace gauge,
+so `MemoryGauge.peak_blocks` is the run's true device footprint in blocks.
+
+PyTorch supplies the memory and the stream; all arithmetic is in
+libbri_b200.so (`_native.py`).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _native
+from .errors import BadPartitionError, DeviceError
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def current_device() -> int:
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise DeviceError("CUDA device required: the BRI hot path runs only on the GPU")
+    return torch.cuda.current_device()
+
+
+def stream_handle(device: int):
+    return ctypes.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
+
+
+def padded_ld(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+class Arena:
+    """nslots device blocks of order n plus a free list and gauge hooks."""
+
+    def __init__(self, n: int, nslots: int, device: int | None = None, gauge=None):
+        torch = _torch()
+        if n < 1 or nslots < 1:
+            raise BadPartitionError(f"arena needs n >= 1 and nslots >= 1, got {n}, {nslots}")
+        self.device = current_device() if device is None else device
+        self.n = n
+        self.ld = padded_ld(n)
+        self.nslots = nslots
+        self.gauge = gauge
+        self.lib = _native.load_library()
+        self.ctx = _native.context(self.device)
+        try:
+            self.tensor = torch.empty((nslots, n, self.ld), dtype=torch.float64, device=f"cuda:{self.device}")
+        except torch.cuda.OutOfMemoryError as e:  # pragma: no cover - depends on device
+            raise BadPartitionError(
+                f"arena of {nslots} blocks of order {n} ({nslots * n * self.ld * 8 / 2**30:.1f} GiB) "
+                f"does not fit in device memory") from e
+        handle = ctypes.c_void_p()
+        _native.check(self.lib.bri_arena_create(self.ctx, ctypes.c_void_p(self.tensor.data_ptr()), n,
+                                                self.ld, nslots, ctypes.byref(handle)), "bri_arena_create")
+        self.handle = handle
+        self._free = list(range(nslots - 1, -1, -1))
+        self._live = set()
+
+    # ------------------------------------------------------------ slots
+    def alloc(self) -> int:
+        if not self._free:
+            raise BadPartitionError(f"arena exhausted ({self.nslots} blocks of order {self.n})")
+        s = self._free.pop()
+        self._live.add(s)
+        if self.gauge is not None:
+            self.gauge.on_alloc()
+        return s
+
+    def release(self, s: int) -> None:
+        self._live.remove(s)
+        self._free.append(s)
+        if self.gauge is not None:
+            self.gauge.on_release()
+
+    def release_all(self) -> None:
+        for s in list(self._live):
+            self.release(s)
+
+    @property
+    def live(self) -> int:
+        return len(self._live)
+
+    def view(self, s: int):
+        """Row-major (n, n) view of slot s (the reference block's layout)."""
+        return self.tensor[s, :, : self.n]
+
+    @property
+    def stream(self):
+        return stream_handle(self.device)
+
+    # ------------------------------------------------------------ ops
+    def _items(self, flat):
+        return _native.int_array(flat)
+
+    def schur(self, items, status) -> None:
+        """items: list of (p, rt, l, r, out, f, w) slot tuples; status: int32 device tensor."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_schur_batch(self.handle, self.stream, len(items), self._items(flat),
+                                               ctypes.c_void_p(status.data_ptr())), "bri_schur_batch")
+
+    def invert(self, items, status) -> None:
+        """items: list of (in, f, out)."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_invert_batch(self.handle, self.stream, len(items), self._items(flat),
+                                                ctypes.c_void_p(status.data_ptr())), "bri_invert_batch")
+
+    def getrf(self, slots, perm, status, ipiv=None) -> None:
+        _native.check(self.lib.bri_getrf_batch(
+            self.handle, self.stream, len(slots), self._items(list(slots)),
+            ctypes.c_void_p(ipiv.data_ptr()) if ipiv is not None else None,
+            ctypes.c_void_p(perm.data_ptr()), ctypes.c_void_p(status.data_ptr())), "bri_getrf_batch")
+
+    def getrs(self, items, perm) -> None:
+        """items: list of (f, src, dst)."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_getrs_batch(self.handle, self.stream, len(items), self._items(flat),
+                                               ctypes.c_void_p(perm.data_ptr())), "bri_getrs_batch")
+
+    def gemm(self, items, M, N, K, a0=(0, 0), b0=(0, 0), c0=(0, 0), alpha=1.0, beta=0.0) -> None:
+        """Column-major window GEMM on slots; items: list of (A, B, C_in, C_out)."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_gemm(self.handle, self.stream, len(items), self._items(flat), M, N, K,
+                                        a0[0], a0[1], b0[0], b0[1], c0[0], c0[1], alpha, beta), "bri_gemm")
+
+    def axpby(self, items, alpha, beta) -> None:
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_axpby(self.handle, self.stream, len(items), self._items(flat),
+                                         alpha, beta), "bri_axpby")
+
+    def transpose(self, items) -> None:
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_transpose(self.handle, self.stream, len(items), self._items(flat)),
+                      "bri_transpose")
+
+    def gather(self, matrix, items) -> None:
+        """Copy blocks of a device row-major matrix: items (block row, block col, slot), 0-based."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_gather_blocks(self.handle, self.stream, ctypes.c_void_p(matrix.data_ptr()),
+                                                 matrix.stride(0), len(items), self._items(flat)),
+                      "bri_gather_blocks")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None:
+            if self.gauge is not None and self._live:
+                self.release_all()
+            self.lib.bri_arena_destroy(self.handle)
+            self.handle = None
+            self.tensor = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            if getattr(self, "handle", None) is not None:
+                self.lib.bri_arena_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def fp64_peak_tflops(iters: int = 4096) -> float:
+    """Measured DMMA throughput of this GPU (register-only mma.sync loop)."""
+    lib = _native.load_library()
+    out = ctypes.c_double()
+    dev = current_device()
+    _native.context(dev)
+    _native.check(lib.bri_fp64_peak(stream_handle(dev), iters, ctypes.byref(out)), "bri_fp64_peak")
+    return out.value

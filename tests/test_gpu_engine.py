@@ -1,0 +1,147 @@
+"""Engine parity against the reference's golden vectors and the CPU oracle (needs a B200)."""
+
+import numpy as np
+import pytest
+
+from conftest import rng, shifted
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bri():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1612_00001_b200 as bri
+
+    return bri
+
+
+def _rel(x, y):
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+
+
+@pytest.mark.parametrize("schedule", ["dag", "tree"])
+def test_worked_example(bri, golden, schedule):
+    data, _ = golden
+    prov = bri.make_memory_provider(np.array([[4.0, 2.0], [1.0, 3.0]]), 2)
+    ws = bri.Workspace(schedule=schedule)
+    for al in (1, 2):
+        for be in (1, 2):
+            out = bri.invert_block(prov, al, be, ws)
+            assert abs(out.data[0, 0] - data[f"worked_{al}{be}"][0, 0]) <= 1e-15
+            out.release()
+    assert ws.gauge.live_blocks == 0
+
+
+@pytest.mark.parametrize("schedule", ["dag", "tree"])
+def test_trace_4x4(bri, golden, schedule):
+    data, meta = golden
+    seen = {}
+    ws = bri.Workspace(schedule=schedule)
+    out = bri.invert_block(bri.make_memory_provider(data["trace4_matrix"], 4), 1, 1, ws,
+                           trace=lambda p, f, v: seen.__setitem__("/".join(q.name for q in p), v))
+    assert list(seen) == meta["trace4_paths"]  # same visiting order as the reference
+    for path in meta["trace4_paths"]:
+        assert abs(seen[path][0, 0] - data[f"trace4_node_{path}"][0, 0]) <= 1e-12
+    assert abs(out.data[0, 0] - data["trace4_out"][0, 0]) <= 1e-12
+
+
+def test_config1_full_inverse(bri, golden):
+    """BASELINE config 1 (k=4, b=64, Uniform[-1,1] + mI, seed 0): all 16 blocks vs the reference."""
+    data, meta = golden
+    a = rng(0).uniform(-1.0, 1.0, (256, 256)) + 256 * np.eye(256)
+    prov = bri.make_memory_provider(a, 4)
+    sink = bri.MemorySink(prov.layout)
+    summ = bri.invert_full(prov, sink)
+    got = sink.finalize()
+    ref = data["cfg1_inverse"]
+    for al in range(4):
+        for be in range(4):
+            blk = slice(al * 64, al * 64 + 64), slice(be * 64, be * 64 + 64)
+            assert _rel(got[blk], ref[blk]) <= 1e-9  # north-star tolerance, per block
+    assert np.abs(a @ got - np.eye(256)).max() <= 1e-12
+    c = summ.counters
+    assert [c.block_inversions, c.block_multiplications, c.block_subtractions, c.schur_nodes] == meta["cfg1_counters"]
+    assert summ.executed.schur_nodes == 116  # distinct DAG nodes
+
+
+def test_random_cases_vs_reference(bri, golden):
+    data, meta = golden
+    for m, k, seed in meta["cases"]:
+        name = f"rand_m{m}_k{k}_s{seed}"
+        prov = bri.make_memory_provider(data[name + "_matrix"], k)
+        keys = [key for key in data.files if key.startswith(name + "_t")]
+        for key in keys:
+            al, be = map(int, key[len(name) + 2:].split("_"))
+            out = bri.invert_block(prov, al, be)
+            assert _rel(out.data, data[key]) <= 1e-9, key
+
+
+def test_spd_k2(bri, golden):
+    data, _ = golden
+    for m in (64, 128):
+        out = bri.invert_block(bri.make_memory_provider(data[f"spd_m{m}_matrix"], 2), 1, 1)
+        assert _rel(out.data, data[f"spd_m{m}_t1_1"]) <= 1e-12
+
+
+@pytest.mark.parametrize("schedule", ["dag", "tree"])
+def test_singular_path(bri, golden, schedule):
+    data, meta = golden
+    with pytest.raises(bri.SingularPivotError) as exc:
+        bri.invert_block(bri.make_memory_provider(data["singular_matrix"], 3), 1, 1,
+                         bri.Workspace(schedule=schedule))
+    assert [q.name for q in exc.value.path] == meta["singular"]["path"]
+    assert list(exc.value.pivot_block) == meta["singular"]["pivot_block"]
+
+
+def test_dag_equals_tree_bitwise(bri):
+    """Memoization changes the schedule, not the arithmetic (b > 96 path)."""
+    a = shifted(128 * 4, 77)
+    prov = bri.make_memory_provider(a, 4)
+    for target in [(1, 1), (2, 3), (4, 1)]:
+        x = bri.invert_block(prov, *target, bri.Workspace(schedule="dag")).data
+        y = bri.invert_block(prov, *target, bri.Workspace(schedule="tree")).data
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_counts_and_tree_footprint(bri, k):
+    ws = bri.Workspace(schedule="tree")
+    prov = bri.make_memory_provider(shifted(k * 4, 82), k)
+    with bri.gauge_scope(ws.gauge) as scope:
+        out = bri.invert_block(prov, 1, 1, ws)
+        out.release()
+    want = bri.predicted_counts(k)
+    assert ws.counters == want
+    assert scope.peak_blocks <= 2 * k + 4
+
+
+def test_block_row_and_full_agree(bri):
+    from oracle import bri_oracle as orc
+
+    a = shifted(6 * 100, 31)
+    prov = bri.make_memory_provider(a, 6)
+    row = bri.invert_block_row(prov, 2)
+    want = orc.invert_full(a, 6, memo=True, targets=[(2, b) for b in range(1, 7)])
+    for b, blk in enumerate(row, start=1):
+        assert _rel(blk.data, want[(2, b)]) <= 1e-9
+
+
+def test_config2_full_size(bri):
+    """BASELINE config 2 at true size: k=2, b=4096, SPD G G^T/m + I, seed 1, block (1,1)."""
+    import torch
+
+    from oracle import bri_oracle as orc
+    from paper_1612_00001_b200.workloads import make_matrix
+
+    a = make_matrix(2)
+    prov = bri.make_memory_provider(a, 2)
+    out = bri.invert_block(prov, 1, 1).data
+    want = orc.invert_block(a, 2, 1, 1)
+    assert _rel(out, want) <= 1e-9
+    # block residual: (M X)[:, block 1] = e_1 block column
+    x_col = np.linalg.solve(a, np.eye(8192)[:, :4096])[:4096]  # dense reference column
+    assert _rel(out, x_col) <= 1e-9

@@ -1,0 +1,147 @@
+"""Host-side logic on CPU: frames, the DAG scheduler, error replay, the C-ABI library surface."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, rng, shifted
+from oracle import bri_oracle as orc
+from paper_1612_00001_b200 import dag, frames, instrumentation, workloads
+from paper_1612_00001_b200.errors import FrameTooSmallError, SingularBlockError, SingularPivotError
+from paper_1612_00001_b200.frames import Quadrant
+
+A, B, C, D = Quadrant.A, Quadrant.B, Quadrant.C, Quadrant.D
+
+
+def test_frames_follow_reference():
+    a, b, c, d = frames.split_frame(frames.root_frame(4))
+    assert (a.rows, a.cols, a.label) == ((1, 2, 3), (1, 2, 3), A)
+    assert (b.rows, b.cols) == ((1, 2, 3), (3, 2, 4))
+    assert (c.rows, c.cols) == ((3, 2, 4), (1, 2, 3))
+    assert (d.rows, d.cols) == ((3, 2, 4), (3, 2, 4))
+    assert frames.frame_at(4, (A, B, C)) == frames.split_frame(frames.split_frame(frames.root_frame(4))[1])[2]
+    with pytest.raises(FrameTooSmallError):
+        frames.split_frame(frames.root_frame(2))
+    with pytest.raises(FrameTooSmallError):
+        frames.frame_at(4, (B,))
+
+    def walk(f):
+        assert f.anchor == (2, 2)
+        if f.n > 2:
+            for ch in frames.split_frame(f):
+                walk(ch)
+
+    walk(frames.root_frame(6))
+    for q in Quadrant:
+        assert q.mirror.mirror is q
+
+
+@pytest.mark.parametrize("k,targets,nodes", [
+    (4, "all", 116), (2, [(1, 1)], 1), (8, "all", 6499), (8, [(1, 1)], 270), (16, [(1, 1)], 3502)])
+def test_dag_sizes_match_survey(k, targets, nodes):
+    tg = [(a, b) for a in range(1, k + 1) for b in range(1, k + 1)] if targets == "all" else targets
+    s = dag.build_schedule(k, tg)
+    assert len(s.nodes) == nodes
+    assert s.tree_nodes(0) == instrumentation.predicted_counts(k).schur_nodes
+
+
+def _emulate(sched, src, fail_on_singular=False):
+    """Evaluate a schedule level by level with the oracle's fold (host emulation of the device run)."""
+    val, pstat = {}, np.zeros(len(sched.nodes), dtype=int)
+    for n, ids in sched.levels().items():
+        for nid in ids:
+            node = sched.nodes[nid]
+            ops = [src.block(r[1], r[2]) if r[0] == "m" else val[r[1]] for r in node.operands]
+            p, rt, l_, r = ops
+            try:
+                inv = orc.invert_dense(p)
+            except orc.OracleSingular as e:
+                pstat[nid] = e.pivot_index
+                val[nid] = np.full_like(p, np.nan)
+                continue
+            val[nid] = r - l_ @ (inv @ rt)
+    return val, pstat
+
+
+@pytest.mark.parametrize("m,k", [(8, 4), (24, 6), (30, 5), (56, 7)])
+def test_dag_schedule_reproduces_tree(m, k):
+    """The scheduler's operand roles and dedup keys reproduce the reference recursion bit for bit."""
+    a = shifted(m, 1000 + m)
+    src = orc.BlockSource(a, k)
+    targets = [(1, 1), (2, k), (k, 3), (k, k)]
+    sched = dag.build_schedule(k, targets)
+    val, pstat = _emulate(sched, src)
+    assert not pstat.any()
+    for t, (al, be) in enumerate(targets):
+        got = orc.invert_dense(val[sched.roots[t]])
+        want = orc.invert_block(a, k, al, be)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_trace_replay_order(golden):
+    data, meta = golden
+    a = data["trace4_matrix"]
+    sched = dag.build_schedule(4, [(1, 1)])
+    val, _ = _emulate(sched, orc.BlockSource(a, 4))
+    seen = []
+    sched.walk(0, on_node=lambda nid, path, fr: seen.append("/".join(q.name for q in path)))
+    assert seen == meta["trace4_paths"]
+
+
+def test_first_failure_replays_reference_path(golden):
+    data, meta = golden
+    a = data["singular_matrix"]
+    sched = dag.build_schedule(3, [(1, 1)])
+    _, pstat = _emulate(sched, orc.BlockSource(a, 3))
+    with pytest.raises(SingularPivotError) as exc:
+        sched.first_failure(pstat, [0], 2)
+    assert [q.name for q in exc.value.path] == meta["singular"]["path"]
+    assert list(exc.value.pivot_block) == meta["singular"]["pivot_block"]
+    with pytest.raises(SingularBlockError):
+        sched.first_failure(np.zeros_like(pstat), [3], 2)
+    sched.first_failure(np.zeros_like(pstat), [0], 2)  # no error
+
+
+def test_workloads_match_reference_generators(golden):
+    data, _ = golden
+    np.testing.assert_array_equal(workloads.make_matrix(1), rng(0).uniform(-1, 1, (256, 256)) + 256 * np.eye(256))
+    c = workloads.config(3)
+    assert (c["k"], c["b"], c["m"], len(c["targets"])) == (8, 1024, 8192, 64)
+    small = workloads.make_matrix(5, b=16)
+    assert small.shape == (128, 128) and small[0, 0] > 100
+    assert workloads.run_flops(4096, 1, 1) == pytest.approx(5.50e11, rel=1e-2)
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "bri_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bri_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_header_symbols():
+    from paper_1612_00001_b200 import _native
+
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libbri_b200.so not built")
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    declared = _declared_symbols()
+    assert len(declared) >= 14
+    for name in declared:
+        assert hasattr(lib, name), name
+    bound = {n for n, _, _ in _native.SIGNATURES}
+    assert bound == set(declared)
+    assert _native.load_library().bri_version() == 100
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_1612_00001_b200 as p
+
+    with pytest.raises(p.DeviceError):
+        p.invert_block(p.make_memory_provider(shifted(8, 1), 2), 1, 1)

@@ -1,0 +1,98 @@
+"""Pin the CPU oracle against golden vectors produced by the reference itself."""
+
+import numpy as np
+import pytest
+
+from conftest import rng, shifted
+from oracle import bri_oracle as orc
+
+
+def _rel(x, y):
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+
+
+def test_worked_example(golden):
+    data, _ = golden
+    a = np.array([[4.0, 2.0], [1.0, 3.0]])
+    for al in (1, 2):
+        for be in (1, 2):
+            got = orc.invert_block(a, 2, al, be)
+            np.testing.assert_array_equal(got, data[f"worked_{al}{be}"])
+    np.testing.assert_allclose(orc.invert_block(a, 2, 1, 1), [[0.3]], atol=1e-15)
+
+
+def test_trace_4x4(golden):
+    data, meta = golden
+    seen = {}
+    out = orc.invert_block(data["trace4_matrix"], 4, 1, 1,
+                           trace=lambda p, f, v: seen.__setitem__("/".join(p), v))
+    assert list(seen) == meta["trace4_paths"]
+    for path in meta["trace4_paths"]:
+        np.testing.assert_array_equal(seen[path], data[f"trace4_node_{path}"])
+    np.testing.assert_array_equal(out, data["trace4_out"])
+    # frozen values from the reference's own test (pkg/tests/test_engine.py:240-241)
+    assert seen["A/B/A"][0, 0] == pytest.approx(-0.280110, abs=1e-6)
+    assert seen["A/B"][0, 0] == pytest.approx(-0.984281, abs=1e-6)
+
+
+@pytest.mark.parametrize("memo", [False, True])
+def test_config1_full_inverse(golden, memo):
+    data, _ = golden
+    a = rng(0).uniform(-1.0, 1.0, (256, 256)) + 256 * np.eye(256)
+    blocks = orc.invert_full(a, 4, memo=memo)
+    full = orc.assemble(blocks, 4, 64)
+    assert _rel(full, data["cfg1_inverse"]) <= 1e-13
+    # memoization is bit-identical to the tree walk
+    if memo:
+        tree = orc.assemble(orc.invert_full(a, 4, memo=False), 4, 64)
+        np.testing.assert_array_equal(full, tree)
+
+
+def test_random_cases(golden):
+    data, meta = golden
+    for m, k, seed in meta["cases"]:
+        name = f"rand_m{m}_k{k}_s{seed}"
+        a = data[name + "_matrix"]
+        np.testing.assert_array_equal(a, shifted(m, seed))
+        for key in data.files:
+            if key.startswith(name + "_t"):
+                al, be = map(int, key[len(name) + 2:].split("_"))
+                got = orc.invert_block(a, k, al, be, memo=True)
+                assert _rel(got, data[key]) <= 1e-13, key
+
+
+def test_spd(golden):
+    data, _ = golden
+    for m in (64, 128):
+        got = orc.invert_block(data[f"spd_m{m}_matrix"], 2, 1, 1)
+        assert _rel(got, data[f"spd_m{m}_t1_1"]) <= 1e-13
+
+
+def test_singular_path(golden):
+    data, meta = golden
+    with pytest.raises(orc.OracleSingularPivot) as exc:
+        orc.invert_block(data["singular_matrix"], 3, 1, 1)
+    assert list(exc.value.path) == meta["singular"]["path"]
+    assert list(exc.value.pivot_block) == meta["singular"]["pivot_block"]
+
+
+def test_dense_kernels(golden):
+    data, _ = golden
+    h = 1.0 / (np.arange(4)[:, None] + np.arange(4)[None, :] + 1.0)
+    np.testing.assert_allclose(orc.invert_dense(h), data["hilbert4_inv"], rtol=1e-12)
+    packed, piv = orc.lu_factor(data["lu6_matrix"])
+    np.testing.assert_array_equal(packed, data["lu6_packed"])
+    np.testing.assert_array_equal(piv, data["lu6_pivots"])
+    for n in (1, 5, 12, 33, 64, 100):
+        got = orc.invert_dense(data[f"inv{n}_matrix"])
+        assert _rel(got, data[f"inv{n}_out"]) <= 1e-14
+
+
+def test_counts(golden):
+    _, meta = golden
+    for k in range(2, 8):
+        nodes = orc.predicted_nodes(k)
+        assert meta["counts"][str(k)] == [nodes + 1, 2 * nodes, nodes, nodes]
+        c = {"nodes": 0, "executed": 0}
+        orc.invert_block(shifted(k, 82), k, 1, 1, counters=c)
+        assert c["nodes"] == nodes and c["executed"] == nodes
