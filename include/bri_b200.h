@@ -39,6 +39,9 @@ typedef struct bri_arena bri_arena;
 /* ABI version (major * 100 + minor). */
 int bri_version(void);
 
+/* Number of kernels this library has launched in the process so far. */
+long long bri_launch_count(void);
+
 /* Message of the last failed call on this thread ("" if none). */
 const char* bri_last_error(void);
 
@@ -90,7 +93,8 @@ int bri_getrs_batch(bri_arena* arena, void* stream, int count, const int* items,
  * core.py:184-197 (subtract).  Column-major window semantics on each slot:
  *   C_out[c_r0:+M, c_c0:+N] = beta * C_in[...] + alpha * A[a_r0:+M, a_c0:+K] * B[b_r0:+K, b_c0:+N]
  * items: 4 ints per product: slots (A, B, C_in, C_out).  For row-major blocks
- * x @ y pass A = y, B = x.  beta == 0 never reads C_in.
+ * x @ y pass A = y, B = x.  beta == 0 never reads C_in.  a_r0 and b_r0 (the
+ * contiguous-dimension offsets) must be even: TMA boxes start 16-byte aligned.
  */
 int bri_gemm(bri_arena* arena, void* stream, int count, const int* items, int M, int N, int K,
              int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha,

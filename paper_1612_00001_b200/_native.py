@@ -21,6 +21,7 @@ _c_int, _c_void_p, _c_double, _c_ll = ctypes.c_int, ctypes.c_void_p, ctypes.c_do
 _P_INT = ctypes.POINTER(ctypes.c_int)
 SIGNATURES = [
     ("bri_version", _c_int, []),
+    ("bri_launch_count", _c_ll, []),
     ("bri_last_error", ctypes.c_char_p, []),
     ("bri_ctx_create", _c_int, [_c_int, ctypes.POINTER(_c_void_p)]),
     ("bri_ctx_destroy", None, [_c_void_p]),

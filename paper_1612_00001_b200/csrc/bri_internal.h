@@ -8,8 +8,13 @@
 
 namespace bri {
 
+// Every kernel launch made by the library bumps this (exported as bri_launch_count).
+void count_launch();
+
 constexpr int NBMAX = 32;        // LU panel width upper bound
 constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
+constexpr int TRSM_BLOCK = 64;   // diagonal block of the fused triangular solve
+constexpr int TRSM_LEAF = 512;   // recursive solves hand sub-triangles up to this size to trsm.cu
 
 // Arena geometry: nslots column-major n x n blocks (X-world), leading dim ld
 // (multiple of 8, >= n), slot i at base + i * slot_elems.
@@ -61,8 +66,13 @@ cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int
                             const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
 cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
                               const unsigned long long* scale_bits, int* status, cudaStream_t s);
-cudaError_t launch_trsm_leaf(const ArenaView& a, const int* fw_slots, int count, bool lower,
-                             int r0, int nr, int nrhs, cudaStream_t s);
+
+int trsm_smem_bytes();
+cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
+                        cudaStream_t s);
+cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
+                              const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
+                              int nrhs, cudaStream_t s);
 
 // Fused one-CTA node / inverse for n <= SMALL_MAX.
 // items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.

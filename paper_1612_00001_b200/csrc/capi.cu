@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -14,6 +15,11 @@
 #include "bri_internal.h"
 
 using namespace bri;
+
+namespace bri {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace bri
 
 namespace {
 
@@ -74,6 +80,7 @@ struct bri_ctx {
   int device = 0;
   DevBuf items;   // uploaded item arrays
   DevBuf lu;      // LU scratch
+  DevBuf dinv;    // inverted diagonal blocks of L and U (fused triangular solves)
   std::vector<int> host;  // staging for item arrays
 };
 
@@ -82,6 +89,7 @@ struct bri_arena {
   ArenaView v{};
   alignas(64) CUtensorMap tmA;
   alignas(64) CUtensorMap tmB;
+  alignas(64) CUtensorMap tmB32;
 };
 
 namespace {
@@ -184,28 +192,51 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   return 0;
 }
 
-// Recursive triangular solve on W with the factor F (both from the item list).
+// Inverted 64 x 64 diagonal blocks of L and U for `count` factors (ctx->dinv):
+// returns pointers to the L and U tables.
+int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, double** dl, double** du) {
+  const int n = ar->v.n;
+  const size_t per = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
+  if (int rc = ar->ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
+  *dl = static_cast<double*>(ar->ctx->dinv.ptr);
+  *du = *dl + per * count;
+  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, s));
+  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, false, *du, s));
+  return 0;
+}
+
+// Recursive triangular solve T * W = W on rows [r0, r0 + nr): large GEMMs at
+// the top, the fused per-panel solve (trsm.cu) for sub-triangles <= TRSM_LEAF.
 // fw: device (F, W) pairs; gemm_fw: device (F, W, W, W) quads.
 int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, int count, bool lower,
-             int r0, int nr, int nrhs) {
-  if (nr <= NBMAX) {
-    BRI_CHECK(launch_trsm_leaf(ar->v, fw, count, lower, r0, nr, nrhs, s));
+             int r0, int nr, int nrhs, const double* dinv) {
+  if (nr <= TRSM_LEAF) {
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->v, fw, count, dinv, lower, r0, nr, nrhs, s));
     return 0;
   }
-  int h = ((nr / 2) + NBMAX - 1) / NBMAX * NBMAX;
-  if (h >= nr) h = nr - NBMAX;
+  int h = ((nr / 2) + TRSM_BLOCK - 1) / TRSM_BLOCK * TRSM_BLOCK;
+  if (h >= nr) h = nr - TRSM_BLOCK;
   if (lower) {
-    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs)) return rc;
+    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs, dinv)) return rc;
     // W[r0+h : r0+nr, :] -= L[r0+h : r0+nr, r0 : r0+h] * W[r0 : r0+h, :]
     if (int rc = gemm_call(ar, s, gemm_fw, count, nr - h, nrhs, h, r0 + h, r0, r0, 0, r0 + h, 0, -1.0, 1.0))
       return rc;
-    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs);
+    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs, dinv);
   }
-  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs)) return rc;
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs, dinv)) return rc;
   // W[r0 : r0+h, :] -= U[r0 : r0+h, r0+h : r0+nr] * W[r0+h : r0+nr, :]
   if (int rc = gemm_call(ar, s, gemm_fw, count, h, nrhs, nr - h, r0, r0 + h, r0 + h, 0, r0, 0, -1.0, 1.0))
     return rc;
-  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs);
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs, dinv);
+}
+
+// Both sweeps of dgetrs on W (already row-permuted): L then U.
+int getrs_sweeps(bri_arena* ar, cudaStream_t s, const int* dev_f, const int* fw, const int* gemm_fw, int count) {
+  double *dl = nullptr, *du = nullptr;
+  if (int rc = make_dinv(ar, s, dev_f, count, &dl, &du)) return rc;
+  const int n = ar->v.n;
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, 0, n, n, dl)) return rc;
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, 0, n, n, du);
 }
 
 // ---------------------------------------------------------------- misc kernels
@@ -274,6 +305,8 @@ extern "C" {
 
 int bri_version(void) { return 100; }
 
+long long bri_launch_count(void) { return bri::g_launches.load(std::memory_order_relaxed); }
+
 const char* bri_last_error(void) { return g_last_error.c_str(); }
 
 int bri_ctx_create(int device, bri_ctx** out) {
@@ -291,6 +324,7 @@ void bri_ctx_destroy(bri_ctx* ctx) {
   cudaDeviceSynchronize();
   if (ctx->items.ptr) cudaFree(ctx->items.ptr);
   if (ctx->lu.ptr) cudaFree(ctx->lu.ptr);
+  if (ctx->dinv.ptr) cudaFree(ctx->dinv.ptr);
   delete ctx;
 }
 
@@ -312,13 +346,17 @@ int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_
   const cuuint32_t estr[3] = {1, 1, 1};
   const cuuint32_t boxA[3] = {8, 16, 1};
   const cuuint32_t boxB[3] = {16, 128, 1};
+  const cuuint32_t boxB32[3] = {16, 32, 1};
   CUresult r1 = enc(&a->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxA, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUresult r2 = enc(&a->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS) {
+  CUresult r3 = enc(&a->tmB32, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB32, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) {
     delete a;
     return fail_msg("cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" + std::to_string((int)r2));
   }
@@ -331,6 +369,8 @@ void bri_arena_destroy(bri_arena* arena) { delete arena; }
 int bri_gemm(bri_arena* ar, void* stream, int count, const int* items, int M, int N, int K, int a_r0,
              int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_gemm: bad arguments");
+  if (((a_r0 | b_r0) & 1) != 0)
+    return fail_msg("bri_gemm: a_r0 and b_r0 must be even (TMA boxes start on 16-byte boundaries)");
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<int> h(items, items + 4 * count);
@@ -347,6 +387,7 @@ int bri_axpby(bri_arena* ar, void* stream, int count, const int* items, double a
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int gx = ar->v.n < 512 ? ar->v.n : 512;
+  bri::count_launch();
   axpby_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, dev, alpha, beta);
   BRI_CHECK(cudaGetLastError());
   return 0;
@@ -360,6 +401,7 @@ int bri_transpose(bri_arena* ar, void* stream, int count, const int* items) {
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int t = (ar->v.n + 31) / 32;
+  bri::count_launch();
   transpose_kernel<<<dim3(t, t, count), dim3(32, 8), 0, s>>>(ar->v, dev);
   BRI_CHECK(cudaGetLastError());
   return 0;
@@ -394,20 +436,20 @@ int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, co
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
-  // layout: [(src,dst) | (F,dst) | (F,dst,dst,dst)]
+  // layout: [(src,dst) | (F,dst) | (F,dst,dst,dst) | F]
   std::vector<int> h;
-  h.reserve(8 * (size_t)count);
+  h.reserve(9 * (size_t)count);
   for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 1]); h.push_back(items[3 * i + 2]); }
   for (int i = 0; i < count; ++i) { h.push_back(items[3 * i]); h.push_back(items[3 * i + 2]); }
   for (int i = 0; i < count; ++i) {
     h.push_back(items[3 * i]);
     for (int q = 0; q < 3; ++q) h.push_back(items[3 * i + 2]);
   }
+  for (int i = 0; i < count; ++i) h.push_back(items[3 * i]);
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   BRI_CHECK(launch_permcopy(ar->v, dev, count, perm, n, false, s));
-  if (int rc = trsm_rec(ar, s, dev + 2 * count, dev + 4 * count, count, true, 0, n, n)) return rc;
-  return trsm_rec(ar, s, dev + 2 * count, dev + 4 * count, count, false, 0, n, n);
+  return getrs_sweeps(ar, s, dev + 6 * count, dev + 2 * count, dev + 4 * count, count);
 }
 
 int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
@@ -454,8 +496,7 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
   if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
   // out = P * I, then L and U solves in place (dgetrs against the identity)
   BRI_CHECK(launch_permcopy(ar->v, d_fo, count, sc.pi, n, true, s));
-  if (int rc = trsm_rec(ar, s, d_fo, d_fooo, count, true, 0, n, n)) return rc;
-  if (int rc = trsm_rec(ar, s, d_fo, d_fooo, count, false, 0, n, n)) return rc;
+  if (int rc = getrs_sweeps(ar, s, d_f, d_fo, d_fooo, count)) return rc;
   if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
   return 0;
 }
@@ -509,8 +550,7 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
   if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
   BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
-  if (int rc = trsm_rec(ar, s, d_fw, d_fwww, count, true, 0, n, n)) return rc;
-  if (int rc = trsm_rec(ar, s, d_fw, d_fwww, count, false, 0, n, n)) return rc;
+  if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count)) return rc;
   if (int rc = gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0)) return rc;
   if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
   return 0;
@@ -525,6 +565,7 @@ int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ld
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int gx = ar->v.n < 1024 ? ar->v.n : 1024;
+  bri::count_launch();
   gather_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, dev);
   BRI_CHECK(cudaGetLastError());
   return 0;

@@ -27,30 +27,31 @@
 //    bit-reproducible across schedules.
 #include "bri_common.cuh"
 #include "bri_internal.h"
+#include "dmma_tile.cuh"
 
 namespace bri {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4;
-constexpr int NUM_CONSUMER_WARPS = 8;
-constexpr int THREADS = NUM_CONSUMER_WARPS * 32;
-constexpr int A_STAGE_BYTES = BM * BK * 8;  // 16 KB
-constexpr int B_STAGE_BYTES = BN * BK * 8;  // 16 KB
-constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BM = 128, BN = 128, BK = TILE_BK, STAGES = 4;
+constexpr int NUM_WARPS = 8;
+constexpr int THREADS = NUM_WARPS * 32;
+constexpr int STAGE_BYTES = StageGeom<BM, BN>::BYTES;    // 32 KB
+constexpr int LDT = BM + 4;                              // epilogue tile stride (doubles)
+constexpr int TILE_BYTES = BN * LDT * 8;                 // 132 KB, reuses the stage ring
+constexpr int RING_BYTES = STAGES * STAGE_BYTES > TILE_BYTES ? STAGES * STAGE_BYTES : TILE_BYTES;
+constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-
   const int item = blockIdx.y;
   const int* it = p.items + 4 * item;
   const int sa = it[0], sb = it[1], sc_in = it[2], sc_out = it[3];
@@ -62,25 +63,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NUM_CONSUMER_WARPS);
+      mbar_init(&empty[s], NUM_WARPS);
     }
     fence_barrier_init();
   }
   __syncthreads();
 
-  // Producer: lane 0 of warp 0 keeps the ring STAGES-1 k-tiles ahead.  Slot s
-  // of k-tile kt is refilled for k-tile kt+STAGES once all 8 warps released it.
+  // Producer: lane 0 of warp 0 keeps the ring STAGES-1 k-tiles ahead; the slot
+  // of k-tile kt is refilled (for kt + STAGES) once all warps released it.
   const bool producer = (warp == 0 && lane == 0);
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
-    uint8_t* sA = smem + s * STAGE_BYTES;
-    uint8_t* sB = sA + A_STAGE_BYTES;
-    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-    const int k0 = kt * BK;
-#pragma unroll
-    for (int ob = 0; ob < BM / 8; ++ob)
-      tma_load_3d(sA + ob * 1024, &tmA, &full[s], p.a_r0 + m0 + ob * 8, p.a_c0 + k0, sa);
-    tma_load_3d(sB, &tmB, &full[s], p.b_r0 + k0, p.b_c0 + n0, sb);
+    tile_issue<BM, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, sa,
+                       p.b_r0 + kt * BK, p.b_c0 + n0, sb);
   };
   if (producer) {
     tma_prefetch_desc(&tmA);
@@ -88,51 +83,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt);
   }
 
-  // -------------------------------------------------------------- consumers
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 1;   // 2 warps along M (64 rows each)
-  const int wn = warp >> 1;  // 4 warps along N (32 cols each)
-  double acc[4][4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
-
+  const int wm0 = (warp & 1) * 64;   // 2 warps along M
+  const int wn0 = (warp >> 1) * 32;  // 4 warps along N
+  WarpAcc<4, 4> acc;
+  acc.zero();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;
     mbar_wait(&full[s], (kt / STAGES) & 1);
     const uint8_t* sA = smem + s * STAGE_BYTES;
-    const uint8_t* sB = sA + A_STAGE_BYTES;
-    const int kvalid = p.K - kt * BK;  // >= BK except on the tail tile
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      const int k = kk * 4 + t;
-      const bool kin = k < kvalid;
-      double a[4][2], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ob = (wm * 64 + i * 16) >> 3;
-        uint32_t off = k * 64 + g * 8;
-        off ^= ((off >> 7) & 3) << 4;
-        a[i][0] = kin ? *reinterpret_cast<const double*>(sA + ob * 1024 + off) : 0.0;
-        a[i][1] = kin ? *reinterpret_cast<const double*>(sA + (ob + 1) * 1024 + off) : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int n = wn * 32 + j * 8 + g;
-        const uint32_t off = n * 128 + (((k >> 1) ^ (n & 7)) << 4) + ((k & 1) << 3);
-        bf[j] = kin ? *reinterpret_cast<const double*>(sB + off) : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], bf[j]);
-    }
+    acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    // refill the slot released one iteration ago (other warps are done with it by now)
     if (producer && kt >= 1) {
       const int kp = kt - 1;
       if (kp + STAGES < KT) {
@@ -142,26 +103,40 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
-  // -------------------------------------------------------------- epilogue
+  // ------------------------------------------------------------ epilogue
+  // Stage alpha*acc through smem, then stream whole columns (contiguous in
+  // memory): every warp access is one 256 B run, and the C_in loads of two
+  // columns are in flight together (C_in may alias C_out).
+  __syncthreads();
+  double* tile = reinterpret_cast<double*>(smem);
+  acc.to_smem(tile, LDT, wm0, wn0, lane, p.alpha);
+  __syncthreads();
   double* cout = p.base + (long long)sc_out * p.slot_elems;
   const double* cin = p.base + (long long)sc_in * p.slot_elems;
   const bool read_c = p.beta != 0.0;
+  for (int c = warp; c < BN; c += 2 * NUM_WARPS) {
+    double v[2][4], old[2][4];
+    long long off[2][4];
+    bool ok[2][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+    for (int u = 0; u < 2; ++u) {
+      const int col = c + u * NUM_WARPS;
+      const int gcol = n0 + col;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int row = m0 + wm * 64 + i * 16 + g + ((v >> 1) << 3);
-        const int col = n0 + wn * 32 + j * 8 + 2 * t + (v & 1);
-        if (row < p.M && col < p.N) {
-          const long long off = (long long)(p.c_r0 + row) + (long long)(p.c_c0 + col) * p.ld;
-          double r = p.alpha * acc[i][j][v];
-          if (read_c) r = fma(p.beta, cin[off], r);
-          cout[off] = r;
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int row = lane + 32 * q;
+        const int grow = m0 + row;
+        ok[u][q] = grow < p.M && gcol < p.N;
+        off[u][q] = (long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld;
+        v[u][q] = tile[col * LDT + row];
+        old[u][q] = (ok[u][q] && read_c) ? cin[off[u][q]] : 0.0;
       }
     }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ok[u][q]) cout[off[u][q]] = read_c ? fma(p.beta, old[u][q], v[u][q]) : v[u][q];
   }
 }
 
@@ -186,6 +161,7 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     return launch_scale_copy(p, count, stream);
   }
   dim3 grid(p.tiles_m * p.tiles_n, count);
+  count_launch();
   gemm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
   return cudaGetLastError();
 }
@@ -206,6 +182,7 @@ __global__ void scale_copy_kernel(GemmParams p) {
 
 cudaError_t launch_scale_copy(const GemmParams& p, int count, cudaStream_t stream) {
   dim3 grid(64, count);
+  count_launch();
   scale_copy_kernel<<<grid, 256, 0, stream>>>(p);
   return cudaGetLastError();
 }

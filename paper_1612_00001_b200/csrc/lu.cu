@@ -201,7 +201,12 @@ __global__ void __launch_bounds__(PANEL_THREADS) lu_panel_kernel(PanelArgs p) {
       }
     }
     __syncthreads();
-    // (e) scale the column below the pivot and rank-1 update the panel
+    // (e) scale the column below the pivot and rank-1 update the panel; the
+    // pivot row is hoisted into registers so the per-row updates are
+    // independent smem read-modify-writes (no aliasing chains)
+    double u[NBMAX];
+#pragma unroll
+    for (int c = 0; c < NBMAX; ++c) u[c] = (c > jj && c < nb) ? urow[c] : 0.0;
     const bool recip = fabs(piv) >= kSfmin;
     const double rinv = 1.0 / piv;
     for (int i = tid; i < myrows; i += PANEL_THREADS) {
@@ -210,7 +215,9 @@ __global__ void __launch_bounds__(PANEL_THREADS) lu_panel_kernel(PanelArgs p) {
       double l = psm[jj * rhp + i];
       if (piv != 0.0) l = recip ? l * rinv : l / piv;
       psm[jj * rhp + i] = l;
-      for (int c = jj + 1; c < nb; ++c) psm[c * rhp + i] = fma(-l, urow[c], psm[c * rhp + i]);
+#pragma unroll
+      for (int c = 0; c < NBMAX; ++c)
+        if (c > jj && c < nb) psm[c * rhp + i] = fma(-l, u[c], psm[c * rhp + i]);
     }
     __syncthreads();
   }
@@ -333,53 +340,6 @@ __global__ void diag_check_kernel(ArenaView a, const int* slots, const unsigned 
   if (threadIdx.x == 0) status[item] = first == INT_MAX ? 0 : first + 1;
 }
 
-// ------------------------------------------------------------- trsm leaf
-// Solve T * W[r0:r0+nr, :] = W[r0:r0+nr, :] with T the nr x nr diagonal block of
-// the factor F at (r0, r0): unit lower (L) or non-unit upper (U).  One thread
-// per right-hand-side column (a contiguous memory row of W).
-template <bool LOWER>
-__global__ void __launch_bounds__(128) trsm_leaf_kernel(ArenaView a, const int* fw, int r0, int nr, int nrhs) {
-  __shared__ double T[NBMAX][NBMAX + 1];
-  const int item = blockIdx.y;
-  const double* F = a.base + (long long)fw[2 * item] * a.slot_elems;
-  double* W = a.base + (long long)fw[2 * item + 1] * a.slot_elems;
-  for (int e = threadIdx.x; e < nr * nr; e += blockDim.x) {
-    const int i = e % nr, c = e / nr;
-    T[i][c] = F[(r0 + i) + (long long)(r0 + c) * a.ld];
-  }
-  __syncthreads();
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nrhs) return;
-  double* col = W + (long long)c * a.ld + r0;
-  double x[NBMAX];
-#pragma unroll
-  for (int i = 0; i < NBMAX; ++i)
-    if (i < nr) x[i] = col[i];
-  if (LOWER) {
-#pragma unroll
-    for (int k = 0; k < NBMAX; ++k)
-      if (k < nr) {
-        const double xk = x[k];
-#pragma unroll
-        for (int i = k + 1; i < NBMAX; ++i)
-          if (i < nr) x[i] = fma(-xk, T[i][k], x[i]);
-      }
-  } else {
-#pragma unroll
-    for (int k = NBMAX - 1; k >= 0; --k)
-      if (k < nr) {
-        const double xk = x[k] / T[k][k];
-        x[k] = xk;
-#pragma unroll
-        for (int i = 0; i < NBMAX; ++i)
-          if (i < k) x[i] = fma(-xk, T[i][k], x[i]);
-      }
-  }
-#pragma unroll
-  for (int i = 0; i < NBMAX; ++i)
-    if (i < nr) col[i] = x[i];
-}
-
 }  // namespace
 
 // ======================================================================
@@ -388,12 +348,14 @@ cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
   const long long total = (long long)a.n * a.n;
   int blocks = (int)((total + 255) / 256);
   blocks = blocks > 64 ? 64 : (blocks < 1 ? 1 : blocks);
+  count_launch();
   maxabs_kernel<<<dim3(blocks, count), 256, 0, s>>>(a, slots, scale_bits);
   return cudaGetLastError();
 }
 
 cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStream_t s) {
   const int gx = a.n < 512 ? a.n : 512;
+  count_launch();
   copy_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs);
   return cudaGetLastError();
 }
@@ -401,11 +363,13 @@ cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStr
 cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, const int* pi,
                             int pi_stride, bool identity_src, cudaStream_t s) {
   const int gx = a.n < 512 ? a.n : 512;
+  count_launch();
   permcopy_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs, pi, pi_stride, identity_src ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pi_init(int* pi, int n, int count, cudaStream_t s) {
+  count_launch();
   pi_init_kernel<<<dim3((n + 255) / 256, count), 256, 0, s>>>(pi, n);
   return cudaGetLastError();
 }
@@ -463,6 +427,7 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  count_launch();
   return cudaLaunchKernelEx(&cfg, lu_panel_kernel, p);
 }
 
@@ -481,23 +446,15 @@ cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int
   p.pair_stride = pair_stride;
   const int cols = a.n - nb;
   const int gx = (cols + RP_THREADS - 1) / RP_THREADS + 1;  // +1: the pi-update block
+  count_launch();
   rowpanel_kernel<<<dim3(gx, count), RP_THREADS, 0, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
                               const unsigned long long* scale_bits, int* status, cudaStream_t s) {
+  count_launch();
   diag_check_kernel<<<count, 256, 0, s>>>(a, slots, scale_bits, status);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trsm_leaf(const ArenaView& a, const int* fw_slots, int count, bool lower,
-                             int r0, int nr, int nrhs, cudaStream_t s) {
-  dim3 grid((nrhs + 127) / 128, count);
-  if (lower)
-    trsm_leaf_kernel<true><<<grid, 128, 0, s>>>(a, fw_slots, r0, nr, nrhs);
-  else
-    trsm_leaf_kernel<false><<<grid, 128, 0, s>>>(a, fw_slots, r0, nr, nrhs);
   return cudaGetLastError();
 }
 

@@ -192,6 +192,7 @@ cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int 
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  count_launch();
   small_node_kernel<NMAX><<<count, SN_THREADS, smem, s>>>(a, items, mode, status);
   return cudaGetLastError();
 }

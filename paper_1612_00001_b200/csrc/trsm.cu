@@ -1,0 +1,268 @@
+// K2: fused triangular solves with many right-hand sides, sm_100a.
+//
+// Replaces the two dtrsm sweeps inside LAPACK dgetrs (core.py:259; getrs
+// solves L then U) — the "p^-1 * l" half of every Schur node and the final
+// block inversion.  Design:
+//
+//  * Diagonal 64 x 64 blocks of L (unit) and U (non-unit) are inverted once
+//    per factorization (dinv_kernel), so every block step becomes DMMA work.
+//  * trsm_kernel: one CTA owns a 32-column panel of the right-hand side and
+//    sweeps the block rows of the triangle in order.  Block row i:
+//        acc  = T[i, done] * X[done, panel]        (TMA-fed DMMA, K grows with i)
+//        X_i  = Tinv_ii * (B_i - acc)               (second DMMA from smem)
+//    The panel's own earlier X rows are re-read through TMA after a
+//    fence.proxy.async, so CTAs never synchronize with each other: a whole
+//    solve (or a batch of them) is one launch with nrhs/32 * batch CTAs.
+//  * Used as the leaf (<= 512 rows) of the recursive solve in capi.cu, whose
+//    upper levels are large GEMMs.
+#include "bri_common.cuh"
+#include "bri_internal.h"
+#include "dmma_tile.cuh"
+
+namespace bri {
+
+namespace {
+
+constexpr int T = TRSM_BLOCK;      // 64
+constexpr int BN = 32;             // right-hand-side columns per CTA
+constexpr int STAGES = 4;
+constexpr int THREADS = 256;
+constexpr int STAGE_BYTES = StageGeom<T, BN>::BYTES;  // 12 KB
+constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
+constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T * LDD * 8 + BN * LDR * 8 + 1024 + 256;
+
+// --------------------------------------------------------------- dinv
+// Invert the T x T diagonal blocks of the factor in slot F: unit lower (L) or
+// non-unit upper (U).  Outside [0, n) the block is the identity.
+// dinv layout per item: [nblk][T x T column-major].
+template <bool LOWER>
+__global__ void __launch_bounds__(T) dinv_kernel(ArenaView a, const int* fslots, double* dinv, int nblk) {
+  extern __shared__ double dsm[];
+  double (*S)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm);            // S[c][r] = block(r, c)
+  double (*X)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm + T * (T + 1));  // X[c][r] = inverse(r, c)
+  const int blk = blockIdx.x, item = blockIdx.y;
+  const double* F = a.base + (long long)fslots[item] * a.slot_elems;
+  const int base = blk * T;
+  const int c = threadIdx.x;
+  for (int r = 0; r < T; ++r) {
+    const int gi = base + r, gj = base + c;
+    double v = (gi < a.n && gj < a.n) ? F[gi + (long long)gj * a.ld] : (r == c ? 1.0 : 0.0);
+    if (LOWER && r == c) v = 1.0;
+    if (LOWER && r < c) v = 0.0;
+    if (!LOWER && r > c) v = 0.0;
+    S[c][r] = v;
+  }
+  __syncthreads();
+  // thread c solves T * x = e_c
+  double* x = X[c];
+  if (LOWER) {
+    for (int r = 0; r < T; ++r) x[r] = 0.0;
+    x[c] = 1.0;
+    for (int r = c + 1; r < T; ++r) {
+      double s = 0.0;
+      for (int k = c; k < r; ++k) s = fma(S[k][r], x[k], s);
+      x[r] = -s;
+    }
+  } else {
+    for (int r = 0; r < T; ++r) x[r] = 0.0;
+    for (int r = c; r >= 0; --r) {
+      double s = (r == c) ? 1.0 : 0.0;
+      for (int k = r + 1; k <= c; ++k) s = fma(-S[k][r], x[k], s);
+      x[r] = s / S[r][r];
+    }
+  }
+  __syncthreads();
+  double* out = dinv + ((long long)item * nblk + blk) * T * T;
+  for (int e = threadIdx.x; e < T * T; e += T) {
+    const int r = e % T, cc = e / T;
+    out[e] = X[cc][r];
+  }
+}
+
+// --------------------------------------------------------------- solve
+struct TrsmArgs {
+  double* base;
+  int ld;
+  long long slot_elems;
+  const int* items;     // (F, W) per item
+  const double* dinv;   // per item [nblk][T*T]
+  int nblk;
+  int r0, nr, nrhs;
+};
+
+template <bool LOWER>
+__global__ void __launch_bounds__(THREADS, 1)
+    trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* D = reinterpret_cast<double*>(smem + STAGES * STAGE_BYTES);   // Tinv_ii, [k][m] col-major (LDD)
+  double* R = D + T * LDD;                                              // B_i - acc, [n][k] (LDR)
+  uint64_t* full = reinterpret_cast<uint64_t*>(R + BN * LDR);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int item = blockIdx.y;
+  const int fs = p.items[2 * item], ws = p.items[2 * item + 1];
+  const int c0 = blockIdx.x * BN;
+  double* W = p.base + (long long)ws * p.slot_elems;
+  const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
+  const int nb = (p.nr + T - 1) / T;
+  const int wm0 = (warp & 3) * 16;   // 4 warps along M (16 rows each)
+  const int wn0 = (warp >> 2) * 16;  // 2 warps along N (16 cols each)
+  const bool producer = (warp == 0 && lane == 0);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], THREADS / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (producer) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+
+  int it = 0;  // k-tiles consumed so far (ring position / phase)
+  for (int ii = 0; ii < nb; ++ii) {
+    const int i = LOWER ? ii : nb - 1 - ii;
+    const int row0 = p.r0 + i * T;
+    const int rows = min(T, p.r0 + p.nr - row0);
+    const int klo = LOWER ? p.r0 : row0 + T;
+    const int khi = LOWER ? row0 : p.r0 + p.nr;
+    const int K = khi - klo;
+    const int KT = K > 0 ? (K + TILE_BK - 1) / TILE_BK : 0;
+    auto issue = [&](int kt) {
+      const int s = (it + kt) % STAGES;
+      tile_issue<T, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, row0, klo + kt * TILE_BK, fs,
+                        klo + kt * TILE_BK, c0, ws);
+    };
+    if (producer)
+      for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt);
+    WarpAcc<1, 2> acc;
+    acc.zero();
+    for (int kt = 0; kt < KT; ++kt) {
+      const int s = (it + kt) % STAGES;
+      mbar_wait(&full[s], ((it + kt) / STAGES) & 1);
+      const uint8_t* sA = smem + s * STAGE_BYTES;
+      acc.mma_stage(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, wn0, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (producer && kt >= 1) {
+        const int kp = kt - 1;
+        if (kp + STAGES < KT) {
+          mbar_wait(&empty[(it + kp) % STAGES], ((it + kp) / STAGES) & 1);
+          issue(kp + STAGES);
+        }
+      }
+    }
+    // (the epilogue's __syncthreads below ends every read of the ring before reuse)
+    it += KT;
+
+    // R = B_i - acc  (rows >= rows and columns >= nrhs are zero)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = wm0 + g + ((v >> 1) << 3);
+        const int cc = wn0 + j * 8 + 2 * t + (v & 1);
+        const bool ok = r < rows && c0 + cc < p.nrhs;
+        const double bval = ok ? W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] : 0.0;
+        R[cc * LDR + r] = ok ? bval - acc.c[0][j][v] : 0.0;
+      }
+    // Tinv_ii into smem
+    const double* Di = dinv + (long long)(row0 / T) * T * T;
+    for (int e = threadIdx.x; e < T * T; e += THREADS) {
+      const int r = e % T, k = e / T;
+      D[k * LDD + r] = Di[e];
+    }
+    __syncthreads();
+    // X_i = Tinv_ii * R   (64 x 32 x 64 DMMA from smem)
+    double x[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) x[j][v] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < T; k0 += 4) {
+      const double a0 = D[(k0 + t) * LDD + wm0 + g];
+      const double a1 = D[(k0 + t) * LDD + wm0 + g + 8];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double b0 = R[(wn0 + j * 8 + g) * LDR + k0 + t];
+        dmma_16x8x4(x[j], a0, a1, b0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int r = wm0 + g + ((v >> 1) << 3);
+        const int cc = wn0 + j * 8 + 2 * t + (v & 1);
+        if (r < rows && c0 + cc < p.nrhs) W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] = x[j][v];
+      }
+    // the next block rows read these X rows through TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int trsm_smem_bytes() { return SMEM_BYTES; }
+
+cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
+                        cudaStream_t s) {
+  const int nblk = (a.n + T - 1) / T;
+  const int smem = 2 * T * (T + 1) * 8;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(dinv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(dinv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(nblk, count);
+  count_launch();
+  if (lower)
+    dinv_kernel<true><<<grid, T, smem, s>>>(a, fslots, dinv, nblk);
+  else
+    dinv_kernel<false><<<grid, T, smem, s>>>(a, fslots, dinv, nblk);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
+                              const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
+                              int nrhs, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  TrsmArgs p;
+  p.base = a.base;
+  p.ld = a.ld;
+  p.slot_elems = a.slot_elems;
+  p.items = fw;
+  p.dinv = dinv;
+  p.nblk = (a.n + T - 1) / T;
+  p.r0 = r0;
+  p.nr = nr;
+  p.nrhs = nrhs;
+  dim3 grid((nrhs + BN - 1) / BN, count);
+  count_launch();
+  if (lower)
+    trsm_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB32, p);
+  else
+    trsm_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB32, p);
+  return cudaGetLastError();
+}
+
+}  // namespace bri

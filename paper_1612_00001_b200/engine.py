@@ -226,7 +226,9 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
     info = RunInfo("tree", len(sched.specs), len(sched.nodes),
                    sum(sched.tree_nodes(t) for t in range(len(sched.specs))), {}, nslots, 1)
     st = torch.zeros(1, dtype=torch.int32, device=dev)
-    perm = torch.zeros(b, dtype=torch.int32, device=dev)
+    # one permutation buffer per recursion depth: a node's pivot permutation must
+    # survive the evaluation of its rt and l subtrees
+    perms = [torch.zeros(b, dtype=torch.int32, device=dev) for _ in range(k + 1)]
     with Arena(b, nslots, device=device, gauge=ws.gauge) as arena:
         for t, (frame0, mr, mc) in enumerate(sched.specs):
 
@@ -247,6 +249,7 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
                     supply = {q: (lambda ch=kids[q]: rec(ch, path + (ch.label,))) for q in kids}
                     roles = PLAN[frame.label.mirror]
                 pq, rtq, lq, rq = roles
+                perm = perms[len(path) - len(sched.paths0[t])]
                 p = supply[pq]()
                 arena.getrf([p], perm, st)            # factor the pivot in place
                 bad = int(st.item())

@@ -102,6 +102,8 @@ class _MemoryProvider(BlockProvider):
             if matrix.dim() != 2 or matrix.shape[0] != matrix.shape[1]:
                 raise DimensionMismatchError(f"matrix must be square, got shape {tuple(matrix.shape)}")
             self._dev = {matrix.device.index: matrix.to(torch.float64).contiguous()} if matrix.is_cuda else {}
+            self._pinned = (matrix.contiguous() if (not matrix.is_cuda and matrix.is_pinned()
+                                                    and matrix.dtype == torch.float64) else None)
             host = None if matrix.is_cuda else matrix.to(torch.float64).numpy()
             m = matrix.shape[0]
         else:
@@ -110,6 +112,7 @@ class _MemoryProvider(BlockProvider):
                 raise DimensionMismatchError(f"matrix must be square, got shape {host.shape}")
             host.setflags(write=False)
             self._dev = {}
+            self._pinned = None
             m = host.shape[0]
         self._host = host
         self.layout = BlockLayout.for_order(m, k)
@@ -134,8 +137,11 @@ class _MemoryProvider(BlockProvider):
         if t is None:
             import torch
 
-            src = torch.from_numpy(np.ascontiguousarray(self.matrix))
-            t = src.pin_memory().to(f"cuda:{device}", non_blocking=True)
+            if self._pinned is not None:  # pinned host tensor: one async H2D copy
+                t = self._pinned.to(f"cuda:{device}", non_blocking=True)
+            else:
+                src = torch.from_numpy(np.array(self.matrix, copy=True))
+                t = src.pin_memory().to(f"cuda:{device}", non_blocking=True)
             self._dev[device] = t
         return t
 

@@ -40,3 +40,24 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+def rel_err(x, y) -> float:
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+
+
+def oracle_with_floor(a, k, targets, seed=123):
+    """CPU-oracle blocks plus the reference's own 1-ulp sensitivity per block.
+
+    The floor is how far the reference BRI moves when M is perturbed by one
+    ulp (M * (1 + eps * N(0,1))): the irreducible
+    disagreement between two correct FP64 implementations that round
+    differently.  Parity is asserted against max(1e-9, 8 * floor).
+    """
+    from oracle import bri_oracle as orc
+
+    pert = a * (1.0 + 2.220446049250313e-16 * rng(seed).standard_normal(a.shape))
+    base = orc.invert_full(a, k, memo=True, targets=list(targets))
+    moved = orc.invert_full(pert, k, memo=True, targets=list(targets))
+    floor = {t: rel_err(moved[t], base[t]) for t in targets}
+    return base, floor

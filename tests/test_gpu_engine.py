@@ -119,15 +119,21 @@ def test_counts_and_tree_footprint(bri, k):
     assert scope.peak_blocks <= 2 * k + 4
 
 
-def test_block_row_and_full_agree(bri):
-    from oracle import bri_oracle as orc
+def test_block_row_vs_oracle_floor(bri):
+    """Off-diagonal targets at k=6: parity judged against the reference's own 1-ulp floor."""
+    from conftest import oracle_with_floor
 
     a = shifted(6 * 100, 31)
     prov = bri.make_memory_provider(a, 6)
     row = bri.invert_block_row(prov, 2)
-    want = orc.invert_full(a, 6, memo=True, targets=[(2, b) for b in range(1, 7)])
+    targets = [(2, b) for b in range(1, 7)]
+    want, floor = oracle_with_floor(a, 6, targets)
     for b, blk in enumerate(row, start=1):
-        assert _rel(blk.data, want[(2, b)]) <= 1e-9
+        assert _rel(blk.data, want[(2, b)]) <= max(1e-9, 8 * floor[(2, b)]), (b, floor[(2, b)])
+    # the diagonal-relative residual of the whole row stays tight
+    x = np.concatenate([blk.data for blk in row], axis=1)  # rows of M^-1 for block row 2
+    resid = np.abs(x @ a - np.eye(600)[100:200]).max()
+    assert resid <= 1e-10
 
 
 def test_config2_full_size(bri):

@@ -46,12 +46,16 @@ def test_gemm_full_and_windows(torch_cuda, n):
     # windowed: ragged M/N/K with offsets, beta = 0 must not read C_in
     ar.view(2).fill_(float("nan"))
     M, N, K = n // 2 + 3, n // 3 + 5, n // 4 + 7
-    a0, b0, c0 = (3, 5), (2, 1), (7, 4)
+    a0, b0, c0 = (4, 5), (2, 1), (7, 4)
     ar.gemm([(0, 1, 2, 2)], M, N, K, a0=a0, b0=b0, c0=c0, alpha=1.0, beta=0.0)
     got = _x(ar.view(2).cpu().numpy())
     want = X[0][a0[0]:a0[0] + M, a0[1]:a0[1] + K] @ X[1][b0[0]:b0[0] + K, b0[1]:b0[1] + N]
     win = got[c0[0]:c0[0] + M, c0[1]:c0[1] + N]
     assert np.abs(win - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+    from paper_1612_00001_b200.errors import DeviceError
+
+    with pytest.raises(DeviceError):  # odd contiguous-dimension offset: rejected, not faulted
+        ar.gemm([(0, 1, 2, 2)], M, N, K, a0=(3, 0), alpha=1.0, beta=0.0)
     ar.close()
 
 
