@@ -449,7 +449,7 @@ int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, co
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   BRI_CHECK(launch_permcopy(ar->v, dev, count, perm, n, false, s));
-  return getrs_sweeps(ar, s, dev + 6 * count, dev + 2 * count, dev + 4 * count, count);
+  return getrs_sweeps(ar, s, dev + 8 * count, dev + 2 * count, dev + 4 * count, count);
 }
 
 int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
