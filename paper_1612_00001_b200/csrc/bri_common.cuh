@@ -139,4 +139,34 @@ BRI_DEVI void warp_argmax(double& v, int& i) {
   }
 }
 
+// Warp-wide argmax of non-negative values with LAPACK idamax tie-breaking
+// (smallest index wins).  Lanes with v < 0 (no candidate) or NaN never win;
+// if no lane has a candidate the result is (-1, INT_MAX).  Three REDUX
+// reductions instead of five shuffle rounds.
+BRI_DEVI void warp_argmax_fast(double& v, int& i) {
+  const bool ok = (v >= 0.0);
+  const unsigned long long bits = ok ? (unsigned long long)__double_as_longlong(v) : 0ull;
+  const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool best = ok && hi == mhi && lo == mlo;
+  const int mi = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)i : 0x7fffffffu);
+  i = mi;
+  v = (mi == 0x7fffffff) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+}
+
+BRI_DEVI double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+BRI_DEVI void lds_f64x2(uint32_t addr, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a), "=d"(b) : "r"(addr));
+}
+
+BRI_DEVI void sts_f64x2(double* p, double a, double b) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(p)), "d"(a), "d"(b) : "memory");
+}
+
 }  // namespace bri

@@ -63,16 +63,19 @@ int panel_width(int n);
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                          const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
 cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
-                            const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
+                            int cbeg, int cend, const LuScratch& sc, int n_stride, int pair_stride,
+                            cudaStream_t s);
+cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
+                         int npan, const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
 cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
                               const unsigned long long* scale_bits, int* status, cudaStream_t s);
 
 int trsm_smem_bytes();
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
-                        cudaStream_t s);
+                        int blk0, int nblocks, cudaStream_t s);
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
                               const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int nrhs, cudaStream_t s);
+                              int c_off, int nrhs, cudaStream_t s);
 
 // Fused one-CTA node / inverse for n <= SMALL_MAX.
 // items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.

@@ -166,25 +166,49 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
   return 0;
 }
 
-// Blocked right-looking LU (dgetrf) of `count` slots in place.
-// gemm_items: device array of 4*count ints (F, F, F, F) per item.
-int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, int count,
-                 const LuLayout& L, const LuScratch& sc) {
+// Blocked right-looking LU (dgetrf) of `count` slots in place, two levels:
+// inner panels of nbi (<= 32) columns factored by the cluster panel kernel and
+// applied inside a 128-wide outer block (rowpanel + rank-nbi GEMM), then the
+// outer block's interchanges, its 128 x 128 triangular solve (fused TRSM) and
+// one rank-128 trailing GEMM — 4x less trailing-matrix traffic than rank-32.
+// dev_slots: F slots; dev_ffff: (F, F, F, F) quads; dev_ff: (F, F) pairs.
+int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, const int* dev_ff,
+                 int count, const LuLayout& L, const LuScratch& sc) {
   const ArenaView& v = ar->v;
   const int n = v.n;
   BRI_CHECK(cudaMemsetAsync(sc.scale_bits, 0, (size_t)count * 8, s));
   BRI_CHECK(cudaMemsetAsync(sc.pairs, 0, (size_t)count * L.pair_stride * 4, s));
   BRI_CHECK(launch_pi_init(sc.pi, n, count, s));
   BRI_CHECK(launch_maxabs(v, dev_slots, count, sc.scale_bits, s));
-  const int nb = panel_width(n);
-  for (int j0 = 0, pidx = 0; j0 < n; j0 += nb, ++pidx) {
-    const int w = (n - j0) < nb ? (n - j0) : nb;
-    BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
-    BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
-    const int rest = n - j0 - w;
+  const int nbi = panel_width(n);
+  const int outer = 128;  // multiple of TRSM_BLOCK and of every inner width
+  const size_t per = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
+  if (int rc = ar->ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
+  double* dl = static_cast<double*>(ar->ctx->dinv.ptr);
+  int pidx = 0;
+  for (int J0 = 0; J0 < n; J0 += outer) {
+    const int W = (n - J0) < outer ? (n - J0) : outer;
+    const int pidx0 = pidx;
+    for (int j0 = J0; j0 < J0 + W; j0 += nbi, ++pidx) {
+      const int w = (J0 + W - j0) < nbi ? (J0 + W - j0) : nbi;
+      BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
+      BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, J0 + W, sc, n, L.pair_stride, s));
+      const int right = J0 + W - j0 - w;
+      if (right > 0 && n - j0 - w > 0) {
+        if (int rc = gemm_call(ar, s, dev_ffff, count, n - j0 - w, right, w, j0 + w, j0, j0, j0 + w, j0 + w,
+                               j0 + w, -1.0, 1.0))
+          return rc;
+      }
+    }
+    BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, pidx - pidx0, sc, n, L.pair_stride, s));
+    const int rest = n - J0 - W;
     if (rest > 0) {
-      if (int rc = gemm_call(ar, s, dev_ffff, count, rest, rest, w, j0 + w, j0, j0, j0 + w, j0 + w,
-                             j0 + w, -1.0, 1.0))
+      const bool aligned = (J0 % TRSM_BLOCK) == 0;
+      if (!aligned) return fail_msg("getrf: outer block not aligned to the TRSM block");
+      BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
+      BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, v, dev_ff, count, dl, true, J0, W, J0 + W, rest, s));
+      if (int rc = gemm_call(ar, s, dev_ffff, count, rest, rest, W, J0 + W, J0, J0, J0 + W, J0 + W, J0 + W,
+                             -1.0, 1.0))
         return rc;
     }
   }
@@ -200,8 +224,8 @@ int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, d
   if (int rc = ar->ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
   *dl = static_cast<double*>(ar->ctx->dinv.ptr);
   *du = *dl + per * count;
-  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, s));
-  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, false, *du, s));
+  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, 0, 0, s));
+  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, false, *du, 0, 0, s));
   return 0;
 }
 
@@ -211,7 +235,7 @@ int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, d
 int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, int count, bool lower,
              int r0, int nr, int nrhs, const double* dinv) {
   if (nr <= TRSM_LEAF) {
-    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->v, fw, count, dinv, lower, r0, nr, nrhs, s));
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->v, fw, count, dinv, lower, r0, nr, 0, nrhs, s));
     return 0;
   }
   int h = ((nr / 2) + TRSM_BLOCK - 1) / TRSM_BLOCK * TRSM_BLOCK;
@@ -413,17 +437,18 @@ int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, in
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
-  std::vector<int> h(5 * (size_t)count);
+  std::vector<int> h(7 * (size_t)count);
   for (int i = 0; i < count; ++i) {
     h[i] = slots[i];
     for (int q = 0; q < 4; ++q) h[count + 4 * i + q] = slots[i];
+    h[5 * count + 2 * i] = h[5 * count + 2 * i + 1] = slots[i];
   }
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   LuLayout L = lu_layout(n, count);
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
-  if (int rc = getrf_device(ar, s, dev, dev + count, count, L, sc)) return rc;
+  if (int rc = getrf_device(ar, s, dev, dev + count, dev + 5 * count, count, L, sc)) return rc;
   if (ipiv) BRI_CHECK(cudaMemcpyAsync(ipiv, sc.ipiv, (size_t)count * n * 4, cudaMemcpyDeviceToDevice, s));
   if (perm) BRI_CHECK(cudaMemcpyAsync(perm, sc.pi, (size_t)count * n * 4, cudaMemcpyDeviceToDevice, s));
   if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
@@ -482,8 +507,10 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
     h.push_back(items[3 * i + 1]);
     for (int q = 0; q < 3; ++q) h.push_back(items[3 * i + 2]);
   }
+  for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 1]); h.push_back(items[3 * i + 1]); }
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_ff = dev + 13 * count;
   const int* d_f = dev;
   const int* d_inf = dev + count;
   const int* d_ffff = dev + 3 * count;
@@ -493,7 +520,7 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
   BRI_CHECK(launch_copy(ar->v, d_inf, count, s));
-  if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
+  if (int rc = getrf_device(ar, s, d_f, d_ffff, d_ff, count, L, sc)) return rc;
   // out = P * I, then L and U solves in place (dgetrs against the identity)
   BRI_CHECK(launch_permcopy(ar->v, d_fo, count, sc.pi, n, true, s));
   if (int rc = getrs_sweeps(ar, s, d_f, d_fo, d_fooo, count)) return rc;
@@ -534,6 +561,7 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
     h.push_back(I(i, 3));
     h.push_back(I(i, 4));
   }
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 5)); h.push_back(I(i, 5)); }
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int* d_f = dev;
@@ -547,7 +575,7 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
   BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
-  if (int rc = getrf_device(ar, s, d_f, d_ffff, count, L, sc)) return rc;
+  if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc)) return rc;
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
   BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
   if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count)) return rc;

@@ -30,7 +30,6 @@ namespace bri {
 namespace {
 
 constexpr int MAXCS = 8;            // cluster size cap (portable)
-constexpr int PANEL_THREADS = 256;
 
 // ----------------------------------------------------------------- maxabs
 __global__ void maxabs_kernel(ArenaView a, const int* slots, unsigned long long* out) {
@@ -87,26 +86,70 @@ __global__ void pi_init_kernel(int* pi, int n) {
 }
 
 // ------------------------------------------------------------------ panel
+// The (n - j0) x nb panel (nb <= 32) is spread over a cluster of cs CTAs of
+// PT threads; thread t of CTA r owns rows row_lo + q*PT + t (q < RPT) and keeps
+// their not-yet-final values in registers, *shifted*: after column jj,
+// x[q][c] holds column jj+1+c.  The shift keeps every register index static
+// while the column loop stays rolled (a fully unrolled panel overflowed the
+// instruction cache: 46% no_instruction stalls).  Finished values — the
+// multipliers (L) of every row and the U rows of the pivots — live in shared
+// memory psm[c * rhp + i] and are written back at the end.  Row buffers are
+// 64 wide with a zero upper half, so shifted reads need no predicates.
+// Per column jj (pivot position j = j0 + jj):
+//   (1) thread candidate, warp shuffle argmax; each warp's winning lane
+//       stores its row (L part from psm by the lanes, live part from its
+//       registers) to wrow[warp]; the owner of row j stores row j -> barrier
+//   (2) every thread picks the CTA winner from the PW slots
+//   (3) cs > 1: warp 0 pushes the CTA candidate row to every CTA (DSMEM),
+//       warp 1 of row j's owner pushes row j -> cluster barrier
+//   (4) every thread picks the global winner; rows j and p are exchanged
+//       (pivot row final in psm); active rows scale and rank-1 update (31 DFMA).
+#ifdef BRI_PANEL_PROFILE
+__device__ unsigned long long g_panel_phase[8];
+#define PPROF(k)                                                         \
+  do {                                                                   \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                           \
+      const unsigned long long now = clock64();                          \
+      g_panel_phase[k] += now - t_last;                                  \
+      t_last = now;                                                      \
+    }                                                                    \
+  } while (0)
+#else
+#define PPROF(k) do { } while (0)
+#endif
+constexpr int PT = 256;
+constexpr int PW = PT / 32;
+constexpr int PNB = NBMAX;      // live register width (narrower panels are zero-padded)
+constexpr int RW = 2 * PNB;     // row buffer width (upper half zero)
+
 struct PanelArgs {
   ArenaView a;
   const int* slots;
-  int j0, nb, rh, rhp, pidx;
+  int j0, nb, rows_per_cta, rhp, pidx;
   int* ipiv;
   int* sigma;
   int* pairs;
   int n_stride, pair_stride;
 };
 
-__global__ void __launch_bounds__(PANEL_THREADS) lu_panel_kernel(PanelArgs p) {
-  extern __shared__ double psm[];  // nb columns x rhp rows, then rhp ints (origins)
-  __shared__ double cand_val[2][MAXCS];
-  __shared__ int cand_idx[2][MAXCS];
-  __shared__ int cand_orig[2][MAXCS];
-  __shared__ double cand_row[2][MAXCS][NBMAX];
-  __shared__ double rowj[2][NBMAX];
-  __shared__ int rowj_orig[2];
-  __shared__ double red_v[PANEL_THREADS / 32];
-  __shared__ int red_i[PANEL_THREADS / 32];
+template <int RPT>
+__global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
+  // Row buffers are split: L part (columns < jj) and the live part in
+  // *shifted* coordinates, x[c] (column jj + c) stored at index c + 1 of a
+  // 34-wide buffer whose tail is zero, so the update reads u[c] = buf[c + 2]
+  // with aligned 16-byte loads.
+  constexpr int SW = 34;
+  extern __shared__ double psm[];                       // nb columns x rhp rows, then rhp ints
+  __shared__ __align__(16) double wL[2][PW][PNB], wS[2][PW][SW];
+  __shared__ double wval[2][PW];
+  __shared__ int widx[2][PW], worig[2][PW];
+  __shared__ __align__(16) double jL[2][PNB], jS[2][SW];
+  __shared__ int jorig_s[2];
+  __shared__ __align__(16) double cL[2][MAXCS][PNB], cS[2][MAXCS][SW];   // cluster candidates
+  __shared__ double cval[2][MAXCS];
+  __shared__ int cidx[2][MAXCS], corig[2][MAXCS];
+  __shared__ __align__(16) double rL[2][PNB], rS[2][SW];                 // row j from its owner CTA
+  __shared__ int rorig[2];
 
   const int cs = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
@@ -115,128 +158,216 @@ __global__ void __launch_bounds__(PANEL_THREADS) lu_panel_kernel(PanelArgs p) {
   double* X = p.a.base + (long long)p.slots[item] * p.a.slot_elems;
   int* orig = reinterpret_cast<int*>(psm + (long long)nb * rhp);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row_lo = j0 + rank * p.rows_per_cta;
+  const int myrows = max(0, min(n, row_lo + p.rows_per_cta) - row_lo);
 
-  const int row_lo = j0 + rank * p.rh;
-  int myrows = n - row_lo;
-  myrows = myrows < 0 ? 0 : (myrows > p.rh ? p.rh : myrows);
+  // zero the shifted buffers (their tails must stay zero)
+  for (int e = tid; e < 2 * PW * SW; e += PT) (&wS[0][0][0])[e] = 0.0;
+  for (int e = tid; e < 2 * MAXCS * SW; e += PT) (&cS[0][0][0])[e] = 0.0;
+  for (int e = tid; e < 2 * SW; e += PT) {
+    (&jS[0][0])[e] = 0.0;
+    (&rS[0][0])[e] = 0.0;
+  }
 
-  // load my slab of the panel (X-columns j0..j0+nb-1 are contiguous memory rows)
-  for (int c = 0; c < nb; ++c)
-    for (int i = tid; i < myrows; i += PANEL_THREADS)
-      psm[c * rhp + i] = X[(row_lo + i) + (long long)(j0 + c) * ld];
-  for (int i = tid; i < myrows; i += PANEL_THREADS) orig[i] = row_lo + i;
+  double x[RPT][PNB];
+  int gi[RPT];
+  bool valid[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int li = q * PT + tid;
+    gi[q] = row_lo + li;
+    valid[q] = li < myrows;
+#pragma unroll
+    for (int c = 0; c < PNB; ++c)
+      x[q][c] = (valid[q] && c < nb) ? X[gi[q] + (long long)(j0 + c) * ld] : 0.0;
+    if (valid[q]) orig[li] = gi[q];
+  }
   if (cs > 1) cluster_sync_all(); else __syncthreads();
+#ifdef BRI_PANEL_PROFILE
+  unsigned long long t_last = clock64();
+#endif
 
   for (int jj = 0; jj < nb; ++jj) {
     const int j = j0 + jj;
     const int par = jj & 1;
-    // (a) CTA-local argmax of |x| over rows >= j
+    // ---- (1) candidates: thread, then warp
     double bv = -1.0;
-    int bi = INT_MAX;
-    for (int i = tid; i < myrows; i += PANEL_THREADS) {
-      const int gi = row_lo + i;
-      if (gi >= j) argmax_merge(bv, bi, fabs(psm[jj * rhp + i]), gi);
-    }
-    warp_argmax(bv, bi);
-    if (lane == 0) {
-      red_v[warp] = bv;
-      red_i[warp] = bi;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      bv = lane < PANEL_THREADS / 32 ? red_v[lane] : -1.0;
-      bi = lane < PANEL_THREADS / 32 ? red_i[lane] : INT_MAX;
-      warp_argmax(bv, bi);
-      const int li = bi - row_lo;
-      const bool have = bi != INT_MAX;
-      for (int d = 0; d < cs; ++d) {
-        if (lane == 0) {
-          dsmem_st_f64(dsmem_addr(&cand_val[par][rank], d), bv);
-          dsmem_st_s32(dsmem_addr(&cand_idx[par][rank], d), bi);
-          dsmem_st_s32(dsmem_addr(&cand_orig[par][rank], d), have ? orig[li] : -1);
-        }
-        if (have && lane < nb)
-          dsmem_st_f64(dsmem_addr(&cand_row[par][rank][lane], d), psm[lane * rhp + li]);
-      }
-    }
-    // (b) the owner of row j publishes it (it is what the pivot row swaps with)
-    if (warp == 1 && j >= row_lo && j < row_lo + myrows) {
-      const int lj = j - row_lo;
-      for (int d = 0; d < cs; ++d) {
-        if (lane < nb) dsmem_st_f64(dsmem_addr(&rowj[par][lane], d), psm[lane * rhp + lj]);
-        if (lane == 0) dsmem_st_s32(dsmem_addr(&rowj_orig[par], d), orig[lj]);
-      }
-    }
-    if (cs > 1) cluster_sync_all(); else __syncthreads();
-
-    // (c) cluster-wide winner (identical in every CTA)
-    double wv = -1.0;
-    int wi = INT_MAX, wr = 0;
-    for (int d = 0; d < cs; ++d) {
-      const double v = cand_val[par][d];
-      const int ix = cand_idx[par][d];
-      if (v > wv || (v == wv && ix < wi)) {
-        wv = v;
-        wi = ix;
-        wr = d;
-      }
-    }
-    const bool none = (wi == INT_MAX);  // all NaN: idamax returns the first index
-    const int pr = none ? j : wi;
-    const double* urow = none ? rowj[par] : cand_row[par][wr];
-    const int uorig = none ? rowj_orig[par] : cand_orig[par][wr];
-    const double piv = urow[jj];
-    if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
-    // (d) interchange rows j and pr (dgetf2 swaps only for a nonzero pivot)
-    if (pr != j && piv != 0.0) {
-      if (j >= row_lo && j < row_lo + myrows) {
-        const int lj = j - row_lo;
-        if (tid < nb) psm[tid * rhp + lj] = urow[tid];
-        if (tid == 0) orig[lj] = uorig;
-      }
-      if (pr >= row_lo && pr < row_lo + myrows) {
-        const int lp = pr - row_lo;
-        if (tid < nb) psm[tid * rhp + lp] = rowj[par][tid];
-        if (tid == 0) orig[lp] = rowj_orig[par];
-      }
-    }
-    __syncthreads();
-    // (e) scale the column below the pivot and rank-1 update the panel; the
-    // pivot row is hoisted into registers so the per-row updates are
-    // independent smem read-modify-writes (no aliasing chains)
-    double u[NBMAX];
+    int bi = INT_MAX, bq = 0;
 #pragma unroll
-    for (int c = 0; c < NBMAX; ++c) u[c] = (c > jj && c < nb) ? urow[c] : 0.0;
+    for (int q = 0; q < RPT; ++q) {
+      if (valid[q] && gi[q] >= j) {
+        const double v = fabs(x[q][0]);
+        if (v > bv || (v == bv && gi[q] < bi)) {
+          bv = v;
+          bi = gi[q];
+          bq = q;
+        }
+      }
+    }
+    double wv = bv;
+    int wi = bi;
+    warp_argmax_fast(wv, wi);
+    PPROF(0);
+    if (wi != INT_MAX) {
+      const int li_w = wi - row_lo;
+      if (lane < jj) wL[par][warp][lane] = psm[lane * rhp + li_w];
+      if (bi == wi) {  // the winning lane stores its live row, shifted
+        double r[PNB];
+#pragma unroll
+        for (int c = 0; c < PNB; ++c) {
+          r[c] = x[0][c];
+#pragma unroll
+          for (int q = 1; q < RPT; ++q)
+            if (bq == q) r[c] = x[q][c];
+        }
+        wS[par][warp][1] = r[0];
+#pragma unroll
+        for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&wS[par][warp][c + 1], r[c], r[c + 1]);
+        wS[par][warp][PNB] = r[PNB - 1];
+        wval[par][warp] = wv;
+        widx[par][warp] = wi;
+        worig[par][warp] = orig[li_w];
+      }
+    } else if (lane == 0) {
+      wval[par][warp] = -1.0;
+      widx[par][warp] = INT_MAX;
+    }
+    const bool own_j = (j >= row_lo && j < row_lo + myrows);
+    const int lj = j - row_lo;
+    if (own_j && warp == ((lj % PT) >> 5)) {
+      if (lane < jj) jL[par][lane] = psm[lane * rhp + lj];
+      if (lane == (lj & 31)) {
+        const int qj = lj / PT;
+        double r[PNB];
+#pragma unroll
+        for (int c = 0; c < PNB; ++c) {
+          r[c] = x[0][c];
+#pragma unroll
+          for (int q = 1; q < RPT; ++q)
+            if (qj == q) r[c] = x[q][c];
+        }
+        jS[par][1] = r[0];
+#pragma unroll
+        for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&jS[par][c + 1], r[c], r[c + 1]);
+        jS[par][PNB] = r[PNB - 1];
+        jorig_s[par] = orig[lj];
+      }
+    }
+    PPROF(1);
+    __syncthreads();
+    PPROF(2);
+    // ---- (2) CTA winner (every warp, one REDUX pass over the PW slots)
+    double cv = wval[par][lane % PW];
+    int ci = widx[par][lane % PW];
+    warp_argmax_fast(cv, ci);
+    const int cw = __ffs(__ballot_sync(0xffffffffu, lane < PW && ci != INT_MAX && widx[par][lane % PW] == ci)) - 1;
+    // ---- (3) cluster exchange
+    uint32_t aL, aS, bL, bS;   // pivot row (L, shifted) and row j (L, shifted)
+    int pr, uorig, jorig;
+    if (cs > 1) {
+      if (warp == 0) {
+        const int w = cw < 0 ? 0 : cw;
+        const double vL = wL[par][w][lane];
+        const double vS = wS[par][w][lane + 1];
+        const int ro = worig[par][w];
+        for (int d = 0; d < cs; ++d) {
+          dsmem_st_f64(dsmem_addr(&cL[par][rank][lane], d), vL);
+          dsmem_st_f64(dsmem_addr(&cS[par][rank][lane + 1], d), vS);
+          if (lane == 0) {
+            dsmem_st_f64(dsmem_addr(&cval[par][rank], d), cv);
+            dsmem_st_s32(dsmem_addr(&cidx[par][rank], d), ci);
+            dsmem_st_s32(dsmem_addr(&corig[par][rank], d), ro);
+          }
+        }
+      } else if (warp == 1 && own_j) {
+        const double vL = jL[par][lane];
+        const double vS = jS[par][lane + 1];
+        const int ro = jorig_s[par];
+        for (int d = 0; d < cs; ++d) {
+          dsmem_st_f64(dsmem_addr(&rL[par][lane], d), vL);
+          dsmem_st_f64(dsmem_addr(&rS[par][lane + 1], d), vS);
+          if (lane == 0) dsmem_st_s32(dsmem_addr(&rorig[par], d), ro);
+        }
+      }
+      cluster_sync_all();
+      double gv = lane < cs ? cval[par][lane] : -1.0;
+      int gidx = lane < cs ? cidx[par][lane] : INT_MAX;
+      warp_argmax_fast(gv, gidx);
+      const int gr = __ffs(__ballot_sync(0xffffffffu, lane < cs && gidx != INT_MAX && cidx[par][lane] == gidx)) - 1;
+      const bool none = gidx == INT_MAX;  // all NaN: idamax returns the first index
+      pr = none ? j : gidx;
+      aL = none ? smem_u32(rL[par]) : smem_u32(cL[par][gr]);
+      aS = none ? smem_u32(rS[par]) : smem_u32(cS[par][gr]);
+      uorig = none ? rorig[par] : corig[par][gr];
+      bL = smem_u32(rL[par]);
+      bS = smem_u32(rS[par]);
+      jorig = rorig[par];
+    } else {
+      const bool none = ci == INT_MAX;
+      pr = none ? j : ci;
+      aL = none ? smem_u32(jL[par]) : smem_u32(wL[par][cw]);
+      aS = none ? smem_u32(jS[par]) : smem_u32(wS[par][cw]);
+      uorig = none ? jorig_s[par] : worig[par][cw];
+      bL = smem_u32(jL[par]);
+      bS = smem_u32(jS[par]);
+      jorig = jorig_s[par];
+    }
+    PPROF(3);
+    // ---- (4) interchange, scale, rank-1 update
+    const double piv = lds_f64(aS + 8);
+    if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
+    const bool swap = (pr != j && piv != 0.0);  // dgetf2 interchanges only for a nonzero pivot
     const bool recip = fabs(piv) >= kSfmin;
     const double rinv = 1.0 / piv;
-    for (int i = tid; i < myrows; i += PANEL_THREADS) {
-      const int gi = row_lo + i;
-      if (gi <= j) continue;
-      double l = psm[jj * rhp + i];
-      if (piv != 0.0) l = recip ? l * rinv : l / piv;
-      psm[jj * rhp + i] = l;
-#pragma unroll
-      for (int c = 0; c < NBMAX; ++c)
-        if (c > jj && c < nb) psm[c * rhp + i] = fma(-l, u[c], psm[c * rhp + i]);
+    if (own_j && warp == ((lj % PT) >> 5)) {    // position j: the pivot row, final
+      const uint32_t sL = swap ? aL : bL, sS = swap ? aS : bS;
+      if (lane < nb) psm[lane * rhp + lj] = lane < jj ? lds_f64(sL + 8 * lane) : lds_f64(sS + 8 * (lane - jj + 1));
+      if (lane == 0 && swap) orig[lj] = uorig;
     }
-    __syncthreads();
+    const bool own_p = swap && pr >= row_lo && pr < row_lo + myrows;
+    const int lp = pr - row_lo;
+    if (own_p && warp == ((lp % PT) >> 5)) {    // position p: old row j's L part
+      if (lane < jj) psm[lane * rhp + lp] = lds_f64(bL + 8 * lane);
+      if (lane == 0) orig[lp] = jorig;
+    }
+    PPROF(4);
+    double u[PNB];
+#pragma unroll
+    for (int c = 0; c < PNB; c += 2) lds_f64x2(aS + 16 + 8 * c, u[c], u[c + 1]);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (!valid[q] || gi[q] <= j) continue;
+      const int li = q * PT + tid;
+      if (own_p && gi[q] == pr) {
+#pragma unroll
+        for (int c = 0; c < PNB; ++c) x[q][c] = lds_f64(bS + 8 * (c + 1));
+      }
+      double l = x[q][0];
+      if (piv != 0.0) l = recip ? l * rinv : l / piv;
+      psm[jj * rhp + li] = l;
+#pragma unroll
+      for (int c = 0; c < PNB - 1; ++c) x[q][c] = fma(-l, u[c], x[q][c + 1]);
+      x[q][PNB - 1] = 0.0;
+    }
+    PPROF(5);
   }
+  __syncthreads();
 
   // write back; publish the interchange map for the rowpanel kernel
-  for (int c = 0; c < nb; ++c)
-    for (int i = tid; i < myrows; i += PANEL_THREADS)
-      X[(row_lo + i) + (long long)(j0 + c) * ld] = psm[c * rhp + i];
+  for (int e = tid; e < nb * myrows; e += PT) {
+    const int c = e / myrows, i = e % myrows;
+    X[(row_lo + i) + (long long)(j0 + c) * ld] = psm[c * rhp + i];
+  }
   int* sig = p.sigma + (long long)item * p.n_stride;
   int* pairs = p.pairs + (long long)item * p.pair_stride + (long long)p.pidx * (1 + 2 * NBMAX);
-  for (int i = tid; i < myrows; i += PANEL_THREADS) {
-    const int gi = row_lo + i;
-    const int o = orig[i];
-    if (gi < j0 + nb) {
-      sig[gi] = o;
-    } else if (o != gi) {
-      const int q = atomicAdd(pairs, 1);
-      pairs[1 + 2 * q] = gi;
-      pairs[2 + 2 * q] = o;
+  for (int i = tid; i < myrows; i += PT) {
+    const int g = row_lo + i, o = orig[i];
+    if (g < j0 + nb) {
+      sig[g] = o;
+    } else if (o != g) {
+      const int k = atomicAdd(pairs, 1);
+      pairs[1 + 2 * k] = g;
+      pairs[2 + 2 * k] = o;
     }
   }
   // no CTA may exit while a peer could still address its shared memory
@@ -244,17 +375,22 @@ __global__ void __launch_bounds__(PANEL_THREADS) lu_panel_kernel(PanelArgs p) {
 }
 
 // --------------------------------------------------------------- rowpanel
+// One warp per X-column outside the panel (a contiguous memory row): apply
+// the panel's interchanges as a gather (all reads before any write, ordered
+// by __syncwarp) and, right of the panel, solve L11 * U12 = A12 across the
+// lanes (lane i owns row j0 + i; forward substitution with shuffles).
 struct RowPanelArgs {
   ArenaView a;
   const int* slots;
   int j0, nb, pidx;
+  int cbeg, cend;     // X-columns handled: [cbeg, cend) minus the panel's own
   const int* sigma;
   const int* pairs;
   int* pi;
   int n_stride, pair_stride;
 };
 
-constexpr int RP_THREADS = 128;
+constexpr int RP_THREADS = 256;
 
 __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
   __shared__ double L[NBMAX][NBMAX + 1];
@@ -264,7 +400,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
   const int n = p.a.n, ld = p.a.ld, nb = p.nb, j0 = p.j0;
   double* X = p.a.base + (long long)p.slots[item] * p.a.slot_elems;
   const int* pairs = p.pairs + (long long)item * p.pair_stride + (long long)p.pidx * (1 + 2 * NBMAX);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < nb) sig[tid] = p.sigma[(long long)item * p.n_stride + j0 + tid];
   if (tid == 0) prs[0] = pairs[0];
   __syncthreads();
@@ -283,43 +419,66 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
     if (tid < cnt) pi[prs[1 + 2 * tid]] = vb;
     return;
   }
-
   for (int e = tid; e < nb * nb; e += RP_THREADS) {
     const int i = e % nb, c = e / nb;
     L[i][c] = X[(j0 + i) + (long long)(j0 + c) * ld];
   }
   __syncthreads();
 
-  const int c = blockIdx.x * RP_THREADS + tid;
-  const int cc = c < j0 ? c : c + nb;  // skip the panel's own columns
-  if (cc >= n) return;
+  const int c = p.cbeg + blockIdx.x * (RP_THREADS / 32) + warp;
+  const bool inside = (j0 >= p.cbeg && j0 < p.cend);
+  const int cc = (inside && c >= j0) ? c + nb : c;  // skip the panel's own columns
+  if (cc >= p.cend || cc >= n) return;
   double* col = X + (long long)cc * ld;
-  double seg[NBMAX];
-  double ov[NBMAX];
-#pragma unroll
-  for (int i = 0; i < NBMAX; ++i)
-    if (i < nb) seg[i] = col[sig[i]];
-#pragma unroll
-  for (int q = 0; q < NBMAX; ++q)
-    if (q < cnt) ov[q] = col[prs[2 + 2 * q]];
-#pragma unroll
-  for (int q = 0; q < NBMAX; ++q)
-    if (q < cnt) col[prs[1 + 2 * q]] = ov[q];
+  const double seg = lane < nb ? col[sig[lane]] : 0.0;
+  const double ov = lane < cnt ? col[prs[2 + 2 * lane]] : 0.0;
+  __syncwarp();
+  if (lane < cnt) col[prs[1 + 2 * lane]] = ov;
+  double xv = seg;
   if (cc >= j0 + nb) {
     // U12 = L11^-1 A12 (dtrsm Left/Lower/NoTrans/Unit order)
-#pragma unroll
-    for (int k = 0; k < NBMAX; ++k) {
-      if (k < nb) {
-        const double xk = seg[k];
-#pragma unroll
-        for (int i = k + 1; i < NBMAX; ++i)
-          if (i < nb) seg[i] = fma(-xk, L[i][k], seg[i]);
-      }
+    for (int k = 0; k < nb - 1; ++k) {
+      const double xk = __shfl_sync(0xffffffffu, xv, k);
+      if (lane > k && lane < nb) xv = fma(-xk, L[lane][k], xv);
     }
   }
-#pragma unroll
-  for (int i = 0; i < NBMAX; ++i)
-    if (i < nb) col[j0 + i] = seg[i];
+  if (lane < nb) col[j0 + lane] = xv;
+}
+
+// ---------------------------------------------------------------- laswp
+// Apply the interchanges of npan consecutive inner panels (starting at panel
+// index pidx0, rows j0q = J0 + q * nbi) to X-columns [0, J0) and [J0 + W, n):
+// one warp per column, each panel as a gather (reads, __syncwarp, writes).
+struct LaswpArgs {
+  ArenaView a;
+  const int* slots;
+  int J0, W, nbi, pidx0, npan;
+  const int* sigma;
+  const int* pairs;
+  int n_stride, pair_stride;
+};
+
+__global__ void __launch_bounds__(RP_THREADS) laswp_kernel(LaswpArgs p) {
+  const int item = blockIdx.y;
+  const int n = p.a.n, ld = p.a.ld;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (RP_THREADS / 32) + warp;
+  const int cc = c < p.J0 ? c : c + p.W;
+  if (cc >= n) return;
+  double* col = p.a.base + (long long)p.slots[item] * p.a.slot_elems + (long long)cc * ld;
+  const int* sig = p.sigma + (long long)item * p.n_stride;
+  for (int q = 0; q < p.npan; ++q) {
+    const int j0 = p.J0 + q * p.nbi;
+    const int w = min(p.nbi, n - j0);
+    const int* pr = p.pairs + (long long)item * p.pair_stride + (long long)(p.pidx0 + q) * (1 + 2 * NBMAX);
+    const int cnt = pr[0];
+    const double seg = lane < w ? col[sig[j0 + lane]] : 0.0;
+    const double ov = lane < cnt ? col[pr[2 + 2 * lane]] : 0.0;
+    __syncwarp();
+    if (lane < cnt) col[pr[1 + 2 * lane]] = ov;
+    if (lane < w) col[j0 + lane] = seg;
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------- diag check
@@ -341,6 +500,14 @@ __global__ void diag_check_kernel(ArenaView a, const int* slots, const unsigned 
 }
 
 }  // namespace
+
+#ifdef BRI_PANEL_PROFILE
+void panel_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_panel_phase, sizeof(g_panel_phase));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_panel_phase, z, sizeof(z));
+}
+#endif
 
 // ======================================================================
 cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
@@ -374,50 +541,23 @@ cudaError_t launch_pi_init(int* pi, int n, int count, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-int panel_width(int n) {
-  // widest panel whose full height fits the distributed smem of an 8-CTA cluster
-  int nb = NBMAX;
-  while (nb > 8 && (long long)n * nb * 8 > (long long)MAXCS * 180 * 1024) nb >>= 1;
-  return nb;
-}
+// Panel width: 32 columns, held in registers (up to 2 rows x 32 per thread).
+int panel_width(int n) { return n > 0 ? NBMAX : NBMAX; }
 
-static int panel_cluster_size(int h, int nb) {
-  // keep a CTA's slab of the panel under ~150 KB of shared memory
-  const long long bytes = (long long)h * nb * 8;
-  int cs = 1;
-  while (cs < MAXCS && bytes > (long long)cs * 150 * 1024) cs *= 2;
-  return cs;
-}
-
-cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
-                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
-  const int h = a.n - j0;
-  const int cs = panel_cluster_size(h, nb);
-  PanelArgs p;
-  p.a = a;
-  p.slots = slots;
-  p.j0 = j0;
-  p.nb = nb;
-  p.pidx = pidx;
-  p.rh = (h + cs - 1) / cs;
-  p.rhp = (p.rh + 1) | 1;  // odd stride: spreads column accesses over banks
-  p.ipiv = sc.ipiv;
-  p.sigma = sc.sigma;
-  p.pairs = sc.pairs;
-  p.n_stride = n_stride;
-  p.pair_stride = pair_stride;
-  const size_t smem = (size_t)nb * p.rhp * 8 + (size_t)p.rhp * 4 + 16;
+template <int RPT>
+static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         200 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         160 * 1024);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)p.nb * p.rhp * 8 + (size_t)p.rhp * 4 + 16;
+  if (smem > 160 * 1024) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(count * cs);
-  cfg.blockDim = dim3(PANEL_THREADS);
+  cfg.blockDim = dim3(PT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -428,26 +568,77 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   count_launch();
-  return cudaLaunchKernelEx(&cfg, lu_panel_kernel, p);
+  return cudaLaunchKernelEx(&cfg, lu_panel_kernel<RPT>, p);
+}
+
+cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
+                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
+  const int h = a.n - j0;
+  // 1 row per thread while it fits a cluster of 8, else 2 (registers: 2 x 32 doubles)
+  const int rpt = h <= MAXCS * PT ? 1 : 2;
+  int cs = 1;
+  while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
+  if ((h + cs - 1) / cs > rpt * PT) return cudaErrorInvalidValue;  // n > 4096: TODO wider clusters
+  PanelArgs p;
+  p.a = a;
+  p.slots = slots;
+  p.j0 = j0;
+  p.nb = nb;
+  p.rows_per_cta = (h + cs - 1) / cs;
+  p.rhp = p.rows_per_cta | 1;
+  p.pidx = pidx;
+  p.ipiv = sc.ipiv;
+  p.sigma = sc.sigma;
+  p.pairs = sc.pairs;
+  p.n_stride = n_stride;
+  p.pair_stride = pair_stride;
+  if (rpt == 1) return launch_panel_t<1>(p, cs, count, s);
+  return launch_panel_t<2>(p, cs, count, s);
 }
 
 cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
-                            const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
+                            int cbeg, int cend, const LuScratch& sc, int n_stride, int pair_stride,
+                            cudaStream_t s) {
   RowPanelArgs p;
   p.a = a;
   p.slots = slots;
   p.j0 = j0;
   p.nb = nb;
   p.pidx = pidx;
+  p.cbeg = cbeg;
+  p.cend = cend;
   p.sigma = sc.sigma;
   p.pairs = sc.pairs;
   p.pi = sc.pi;
   p.n_stride = n_stride;
   p.pair_stride = pair_stride;
-  const int cols = a.n - nb;
-  const int gx = (cols + RP_THREADS - 1) / RP_THREADS + 1;  // +1: the pi-update block
+  const int cols = (cend - cbeg) - ((j0 >= cbeg && j0 < cend) ? nb : 0);
+  const int wpb = RP_THREADS / 32;
+  const int gx = (cols + wpb - 1) / wpb + 1;  // +1: the pi-update block
   count_launch();
   rowpanel_kernel<<<dim3(gx, count), RP_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
+                        int npan, const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
+  const int cols = a.n - W;
+  if (cols <= 0) return cudaSuccess;
+  LaswpArgs p;
+  p.a = a;
+  p.slots = slots;
+  p.J0 = J0;
+  p.W = W;
+  p.nbi = nbi;
+  p.pidx0 = pidx0;
+  p.npan = npan;
+  p.sigma = sc.sigma;
+  p.pairs = sc.pairs;
+  p.n_stride = n_stride;
+  p.pair_stride = pair_stride;
+  const int wpb = RP_THREADS / 32;
+  count_launch();
+  laswp_kernel<<<dim3((cols + wpb - 1) / wpb, count), RP_THREADS, 0, s>>>(p);
   return cudaGetLastError();
 }
 

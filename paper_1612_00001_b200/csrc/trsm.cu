@@ -37,11 +37,11 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T * LDD * 8 + BN * LDR * 8 + 1
 // non-unit upper (U).  Outside [0, n) the block is the identity.
 // dinv layout per item: [nblk][T x T column-major].
 template <bool LOWER>
-__global__ void __launch_bounds__(T) dinv_kernel(ArenaView a, const int* fslots, double* dinv, int nblk) {
+__global__ void __launch_bounds__(T) dinv_kernel(ArenaView a, const int* fslots, double* dinv, int nblk, int blk0) {
   extern __shared__ double dsm[];
   double (*S)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm);            // S[c][r] = block(r, c)
   double (*X)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm + T * (T + 1));  // X[c][r] = inverse(r, c)
-  const int blk = blockIdx.x, item = blockIdx.y;
+  const int blk = blk0 + blockIdx.x, item = blockIdx.y;
   const double* F = a.base + (long long)fslots[item] * a.slot_elems;
   const int base = blk * T;
   const int c = threadIdx.x;
@@ -88,7 +88,7 @@ struct TrsmArgs {
   const int* items;     // (F, W) per item
   const double* dinv;   // per item [nblk][T*T]
   int nblk;
-  int r0, nr, nrhs;
+  int r0, nr, c_off, nrhs;
 };
 
 template <bool LOWER>
@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int g = lane >> 2, t = lane & 3;
   const int item = blockIdx.y;
   const int fs = p.items[2 * item], ws = p.items[2 * item + 1];
-  const int c0 = blockIdx.x * BN;
+  const int c0 = p.c_off + blockIdx.x * BN;
+  const int cend = p.c_off + p.nrhs;
   double* W = p.base + (long long)ws * p.slot_elems;
   const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
   const int nb = (p.nr + T - 1) / T;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int v = 0; v < 4; ++v) {
         const int r = wm0 + g + ((v >> 1) << 3);
         const int cc = wn0 + j * 8 + 2 * t + (v & 1);
-        const bool ok = r < rows && c0 + cc < p.nrhs;
+        const bool ok = r < rows && c0 + cc < cend;
         const double bval = ok ? W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] : 0.0;
         R[cc * LDR + r] = ok ? bval - acc.c[0][j][v] : 0.0;
       }
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int v = 0; v < 4; ++v) {
         const int r = wm0 + g + ((v >> 1) << 3);
         const int cc = wn0 + j * 8 + 2 * t + (v & 1);
-        if (r < rows && c0 + cc < p.nrhs) W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] = x[j][v];
+        if (r < rows && c0 + cc < cend) W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] = x[j][v];
       }
     // the next block rows read these X rows through TMA (async proxy)
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -215,8 +216,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 int trsm_smem_bytes() { return SMEM_BYTES; }
 
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
-                        cudaStream_t s) {
+                        int blk0, int nblocks, cudaStream_t s) {
   const int nblk = (a.n + T - 1) / T;
+  if (nblocks <= 0) nblocks = nblk - blk0;
   const int smem = 2 * T * (T + 1) * 8;
   static bool configured = false;
   if (!configured) {
@@ -226,18 +228,18 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid(nblk, count);
+  dim3 grid(nblocks, count);
   count_launch();
   if (lower)
-    dinv_kernel<true><<<grid, T, smem, s>>>(a, fslots, dinv, nblk);
+    dinv_kernel<true><<<grid, T, smem, s>>>(a, fslots, dinv, nblk, blk0);
   else
-    dinv_kernel<false><<<grid, T, smem, s>>>(a, fslots, dinv, nblk);
+    dinv_kernel<false><<<grid, T, smem, s>>>(a, fslots, dinv, nblk, blk0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
                               const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int nrhs, cudaStream_t s) {
+                              int c_off, int nrhs, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -255,6 +257,7 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
   p.nblk = (a.n + T - 1) / T;
   p.r0 = r0;
   p.nr = nr;
+  p.c_off = c_off;
   p.nrhs = nrhs;
   dim3 grid((nrhs + BN - 1) / BN, count);
   count_launch();
