@@ -78,6 +78,11 @@ def _dev(ws) -> str:
     return f"cuda:{d}"
 
 
+def _to_host(t) -> np.ndarray:
+    """D2H into a fresh host tensor; the ndarray shares (and keeps alive) its memory."""
+    return t.detach().cpu().numpy()
+
+
 class Block:
     """One square float64 block resident in device memory."""
 
@@ -120,7 +125,7 @@ class Block:
     def data(self) -> np.ndarray:
         """Host copy (numpy, C-ordered); refreshed after device-side updates."""
         if self._host is None:
-            self._host = self._t.detach().cpu().numpy().copy()
+            self._host = _to_host(self._t)
         return self._host
 
     def _touch(self) -> None:

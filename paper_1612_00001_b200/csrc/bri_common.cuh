@@ -155,6 +155,33 @@ BRI_DEVI void warp_argmax_fast(double& v, int& i) {
   v = (mi == 0x7fffffff) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
 }
 
+// st.async: remote (cluster) shared store that signals `bytes` on the
+// destination CTA's mbarrier (complete_tx); both addresses are shared::cluster.
+BRI_DEVI void st_async_f64(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(mbar)
+               : "memory");
+}
+
+BRI_DEVI void st_async_s32(uint32_t addr, int v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+               "r"(mbar)
+               : "memory");
+}
+
+BRI_DEVI void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAITC_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 BRI_DEVI double lds_f64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));

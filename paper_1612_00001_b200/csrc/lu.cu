@@ -32,24 +32,26 @@ namespace {
 constexpr int MAXCS = 8;            // cluster size cap (portable)
 
 // ----------------------------------------------------------------- maxabs
+// max |X| per slot (the scale of the singularity test, core.py:200-209).  One
+// CTA row per X-column group, coalesced along the contiguous dimension; the
+// bit-pattern max lets NaN (positive, above +Inf) propagate like numpy's max.
 __global__ void maxabs_kernel(ArenaView a, const int* slots, unsigned long long* out) {
   const int item = blockIdx.y;
   const double* x = a.base + (long long)slots[item] * a.slot_elems;
-  double best = 0.0;
-  const long long total = (long long)a.n * a.n;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e % a.n), j = (int)(e / a.n);
-    const double v = fabs(x[i + (long long)j * a.ld]);
-    // bit-pattern max: NaN (positive, > +Inf bits) propagates like numpy's max
-    if (__double_as_longlong(v) > __double_as_longlong(best)) best = v;
+  long long best = 0;
+  for (int j = blockIdx.x; j < a.n; j += gridDim.x) {
+    const double* col = x + (long long)j * a.ld;
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) {
+      const long long v = __double_as_longlong(fabs(col[i]));
+      best = v > best ? v : best;
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    const double o = __shfl_xor_sync(0xffffffffu, best, off);
-    if (__double_as_longlong(o) > __double_as_longlong(best)) best = o;
+    const long long o = __shfl_xor_sync(0xffffffffu, best, off);
+    best = o > best ? o : best;
   }
-  if ((threadIdx.x & 31) == 0) atomicMax(out + item, (unsigned long long)__double_as_longlong(best));
+  if ((threadIdx.x & 31) == 0) atomicMax(out + item, (unsigned long long)best);
 }
 
 // ------------------------------------------------------------------- copy
@@ -132,6 +134,25 @@ struct PanelArgs {
   int n_stride, pair_stride;
 };
 
+
+// The owning lane stores its live row, shifted (x[c] -> dst[c + 1]), with
+// 16-byte stores; dst is a 16-byte aligned 34-wide buffer (tail stays zero).
+template <int RPT>
+BRI_DEVI void store_live_row(double* dst, const double (&x)[RPT][PNB], int q) {
+  double r[PNB];
+#pragma unroll
+  for (int c = 0; c < PNB; ++c) {
+    r[c] = x[0][c];
+#pragma unroll
+    for (int qq = 1; qq < RPT; ++qq)
+      if (q == qq) r[c] = x[qq][c];
+  }
+  dst[1] = r[0];
+#pragma unroll
+  for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&dst[c + 1], r[c], r[c + 1]);
+  dst[PNB] = r[PNB - 1];
+}
+
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   // Row buffers are split: L part (columns < jj) and the live part in
@@ -140,16 +161,15 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   // with aligned 16-byte loads.
   constexpr int SW = 34;
   extern __shared__ double psm[];                       // nb columns x rhp rows, then rhp ints
-  __shared__ __align__(16) double wL[2][PW][PNB], wS[2][PW][SW];
   __shared__ double wval[2][PW];
-  __shared__ int widx[2][PW], worig[2][PW];
-  __shared__ __align__(16) double jL[2][PNB], jS[2][SW];
-  __shared__ int jorig_s[2];
-  __shared__ __align__(16) double cL[2][MAXCS][PNB], cS[2][MAXCS][SW];   // cluster candidates
+  __shared__ int widx[2][PW];
+  __shared__ __align__(16) double cL[2][MAXCS][PNB], cS[2][MAXCS][SW];   // candidates (per source CTA)
   __shared__ double cval[2][MAXCS];
   __shared__ int cidx[2][MAXCS], corig[2][MAXCS];
-  __shared__ __align__(16) double rL[2][PNB], rS[2][SW];                 // row j from its owner CTA
+  __shared__ __align__(16) double rL[2][PNB], rS[2][SW];                 // row j (from its owner CTA)
   __shared__ int rorig[2];
+  __shared__ __align__(8) uint64_t xbar[2];                              // exchange mbarriers (cs > 1)
+  __shared__ __align__(16) double stS[2][SW], stJ[2][SW];               // local staging (cs > 1)
 
   const int cs = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
@@ -160,13 +180,15 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row_lo = j0 + rank * p.rows_per_cta;
   const int myrows = max(0, min(n, row_lo + p.rows_per_cta) - row_lo);
+  // bytes each CTA receives per column: cs candidates + row j
+  const uint32_t xbytes = (uint32_t)cs * (2 * PNB * 8 + 8 + 4 + 4) + (2 * PNB * 8 + 4);
 
-  // zero the shifted buffers (their tails must stay zero)
-  for (int e = tid; e < 2 * PW * SW; e += PT) (&wS[0][0][0])[e] = 0.0;
   for (int e = tid; e < 2 * MAXCS * SW; e += PT) (&cS[0][0][0])[e] = 0.0;
-  for (int e = tid; e < 2 * SW; e += PT) {
-    (&jS[0][0])[e] = 0.0;
-    (&rS[0][0])[e] = 0.0;
+  for (int e = tid; e < 2 * SW; e += PT) (&rS[0][0])[e] = 0.0;
+  if (tid == 0) {
+    mbar_init(&xbar[0], 1);
+    mbar_init(&xbar[1], 1);
+    fence_barrier_init();
   }
 
   double x[RPT][PNB];
@@ -182,6 +204,21 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
       x[q][c] = (valid[q] && c < nb) ? X[gi[q] + (long long)(j0 + c) * ld] : 0.0;
     if (valid[q]) orig[li] = gi[q];
   }
+  // candidate for column 0
+  double bv = -1.0;
+  int bi = INT_MAX, bq = 0;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q)
+    if (valid[q]) {
+      const double v = fabs(x[q][0]);
+      if (v > bv || (v == bv && gi[q] < bi)) { bv = v; bi = gi[q]; bq = q; }
+    }
+  {
+    double wv = bv;
+    int wi = bi;
+    warp_argmax_fast(wv, wi);
+    if (lane == 0) { wval[0][warp] = wv; widx[0][warp] = wi; }
+  }
   if (cs > 1) cluster_sync_all(); else __syncthreads();
 #ifdef BRI_PANEL_PROFILE
   unsigned long long t_last = clock64();
@@ -190,106 +227,65 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   for (int jj = 0; jj < nb; ++jj) {
     const int j = j0 + jj;
     const int par = jj & 1;
-    // ---- (1) candidates: thread, then warp
-    double bv = -1.0;
-    int bi = INT_MAX, bq = 0;
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-      if (valid[q] && gi[q] >= j) {
-        const double v = fabs(x[q][0]);
-        if (v > bv || (v == bv && gi[q] < bi)) {
-          bv = v;
-          bi = gi[q];
-          bq = q;
-        }
-      }
-    }
-    double wv = bv;
-    int wi = bi;
-    warp_argmax_fast(wv, wi);
-    PPROF(0);
-    if (wi != INT_MAX) {
-      const int li_w = wi - row_lo;
-      if (lane < jj) wL[par][warp][lane] = psm[lane * rhp + li_w];
-      if (bi == wi) {  // the winning lane stores its live row, shifted
-        double r[PNB];
-#pragma unroll
-        for (int c = 0; c < PNB; ++c) {
-          r[c] = x[0][c];
-#pragma unroll
-          for (int q = 1; q < RPT; ++q)
-            if (bq == q) r[c] = x[q][c];
-        }
-        wS[par][warp][1] = r[0];
-#pragma unroll
-        for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&wS[par][warp][c + 1], r[c], r[c + 1]);
-        wS[par][warp][PNB] = r[PNB - 1];
-        wval[par][warp] = wv;
-        widx[par][warp] = wi;
-        worig[par][warp] = orig[li_w];
-      }
-    } else if (lane == 0) {
-      wval[par][warp] = -1.0;
-      widx[par][warp] = INT_MAX;
-    }
-    const bool own_j = (j >= row_lo && j < row_lo + myrows);
-    const int lj = j - row_lo;
-    if (own_j && warp == ((lj % PT) >> 5)) {
-      if (lane < jj) jL[par][lane] = psm[lane * rhp + lj];
-      if (lane == (lj & 31)) {
-        const int qj = lj / PT;
-        double r[PNB];
-#pragma unroll
-        for (int c = 0; c < PNB; ++c) {
-          r[c] = x[0][c];
-#pragma unroll
-          for (int q = 1; q < RPT; ++q)
-            if (qj == q) r[c] = x[q][c];
-        }
-        jS[par][1] = r[0];
-#pragma unroll
-        for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&jS[par][c + 1], r[c], r[c + 1]);
-        jS[par][PNB] = r[PNB - 1];
-        jorig_s[par] = orig[lj];
-      }
-    }
-    PPROF(1);
-    __syncthreads();
-    PPROF(2);
-    // ---- (2) CTA winner (every warp, one REDUX pass over the PW slots)
+    if (cs > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[par], xbytes);
+    // ---- (2) CTA winner from the warp slots (written at the end of the previous column)
     double cv = wval[par][lane % PW];
     int ci = widx[par][lane % PW];
     warp_argmax_fast(cv, ci);
-    const int cw = __ffs(__ballot_sync(0xffffffffu, lane < PW && ci != INT_MAX && widx[par][lane % PW] == ci)) - 1;
-    // ---- (3) cluster exchange
-    uint32_t aL, aS, bL, bS;   // pivot row (L, shifted) and row j (L, shifted)
+    PPROF(0);
+    // ---- (3) publish: the CTA winner's row and row j, by their owning warps
+    const bool have = ci != INT_MAX;
+    const int lw = ci - row_lo;                    // local index of the CTA winner
+    const bool own_j = (j >= row_lo && j < row_lo + myrows);
+    const int lj = j - row_lo;
+    uint32_t aL, aS, bL, bS;
     int pr, uorig, jorig;
     if (cs > 1) {
-      if (warp == 0) {
-        const int w = cw < 0 ? 0 : cw;
-        const double vL = wL[par][w][lane];
-        const double vS = wS[par][w][lane + 1];
-        const int ro = worig[par][w];
+      // every destination (incl. ourselves) receives our candidate in slot `rank`
+      if (have && warp == ((lw % PT) >> 5)) {
+        if (lane == (lw & 31)) store_live_row<RPT>(stS[par], x, lw / PT);
+        __syncwarp();
+        const double sv = stS[par][lane + 1];
+        const double lv = lane < jj ? psm[lane * rhp + lw] : 0.0;
+        const int ro = orig[lw];
         for (int d = 0; d < cs; ++d) {
-          dsmem_st_f64(dsmem_addr(&cL[par][rank][lane], d), vL);
-          dsmem_st_f64(dsmem_addr(&cS[par][rank][lane + 1], d), vS);
+          const uint32_t mb = dsmem_addr(&xbar[par], d);
+          st_async_f64(dsmem_addr(&cL[par][rank][lane], d), lv, mb);
+          st_async_f64(dsmem_addr(&cS[par][rank][lane + 1], d), sv, mb);
           if (lane == 0) {
-            dsmem_st_f64(dsmem_addr(&cval[par][rank], d), cv);
-            dsmem_st_s32(dsmem_addr(&cidx[par][rank], d), ci);
-            dsmem_st_s32(dsmem_addr(&corig[par][rank], d), ro);
+            st_async_f64(dsmem_addr(&cval[par][rank], d), cv, mb);
+            st_async_s32(dsmem_addr(&cidx[par][rank], d), ci, mb);
+            st_async_s32(dsmem_addr(&corig[par][rank], d), ro, mb);
           }
         }
-      } else if (warp == 1 && own_j) {
-        const double vL = jL[par][lane];
-        const double vS = jS[par][lane + 1];
-        const int ro = jorig_s[par];
+      } else if (!have && warp == 0) {
         for (int d = 0; d < cs; ++d) {
-          dsmem_st_f64(dsmem_addr(&rL[par][lane], d), vL);
-          dsmem_st_f64(dsmem_addr(&rS[par][lane + 1], d), vS);
-          if (lane == 0) dsmem_st_s32(dsmem_addr(&rorig[par], d), ro);
+          const uint32_t mb = dsmem_addr(&xbar[par], d);
+          st_async_f64(dsmem_addr(&cL[par][rank][lane], d), 0.0, mb);
+          st_async_f64(dsmem_addr(&cS[par][rank][lane + 1], d), 0.0, mb);
+          if (lane == 0) {
+            st_async_f64(dsmem_addr(&cval[par][rank], d), -1.0, mb);
+            st_async_s32(dsmem_addr(&cidx[par][rank], d), INT_MAX, mb);
+            st_async_s32(dsmem_addr(&corig[par][rank], d), -1, mb);
+          }
         }
       }
-      cluster_sync_all();
+      if (own_j && warp == ((lj % PT) >> 5)) {
+        if (lane == (lj & 31)) store_live_row<RPT>(stJ[par], x, lj / PT);
+        __syncwarp();
+        const double sv = stJ[par][lane + 1];
+        const double lv = lane < jj ? psm[lane * rhp + lj] : 0.0;
+        const int ro = orig[lj];
+        for (int d = 0; d < cs; ++d) {
+          const uint32_t mb = dsmem_addr(&xbar[par], d);
+          st_async_f64(dsmem_addr(&rL[par][lane], d), lv, mb);
+          st_async_f64(dsmem_addr(&rS[par][lane + 1], d), sv, mb);
+          if (lane == 0) st_async_s32(dsmem_addr(&rorig[par], d), ro, mb);
+        }
+      }
+      PPROF(1);
+      mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);
+      PPROF(2);
       double gv = lane < cs ? cval[par][lane] : -1.0;
       int gidx = lane < cs ? cidx[par][lane] : INT_MAX;
       warp_argmax_fast(gv, gidx);
@@ -299,21 +295,36 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
       aL = none ? smem_u32(rL[par]) : smem_u32(cL[par][gr]);
       aS = none ? smem_u32(rS[par]) : smem_u32(cS[par][gr]);
       uorig = none ? rorig[par] : corig[par][gr];
-      bL = smem_u32(rL[par]);
-      bS = smem_u32(rS[par]);
       jorig = rorig[par];
     } else {
-      const bool none = ci == INT_MAX;
-      pr = none ? j : ci;
-      aL = none ? smem_u32(jL[par]) : smem_u32(wL[par][cw]);
-      aS = none ? smem_u32(jS[par]) : smem_u32(wS[par][cw]);
-      uorig = none ? jorig_s[par] : worig[par][cw];
-      bL = smem_u32(jL[par]);
-      bS = smem_u32(jS[par]);
-      jorig = jorig_s[par];
+      if (have && warp == ((lw % PT) >> 5)) {
+        if (lane == (lw & 31)) {
+          store_live_row<RPT>(cS[par][0], x, lw / PT);
+          corig[par][0] = orig[lw];
+        }
+        if (lane < jj) cL[par][0][lane] = psm[lane * rhp + lw];
+      }
+      if (own_j && warp == ((lj % PT) >> 5)) {
+        if (lane == (lj & 31)) {
+          store_live_row<RPT>(rS[par], x, lj / PT);
+          rorig[par] = orig[lj];
+        }
+        if (lane < jj) rL[par][lane] = psm[lane * rhp + lj];
+      }
+      PPROF(1);
+      __syncthreads();
+      PPROF(2);
+      pr = have ? ci : j;
+      aL = have ? smem_u32(cL[par][0]) : smem_u32(rL[par]);
+      aS = have ? smem_u32(cS[par][0]) : smem_u32(rS[par]);
+      uorig = have ? corig[par][0] : rorig[par];
+      jorig = rorig[par];
     }
+    bL = smem_u32(rL[par]);
+    bS = smem_u32(rS[par]);
     PPROF(3);
-    // ---- (4) interchange, scale, rank-1 update
+    // ---- (4) interchange, scale, rank-1 update; the next column's candidate
+    //          is formed as soon as its values are updated
     const double piv = lds_f64(aS + 8);
     if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
     const bool swap = (pr != j && piv != 0.0);  // dgetf2 interchanges only for a nonzero pivot
@@ -334,24 +345,46 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     double u[PNB];
 #pragma unroll
     for (int c = 0; c < PNB; c += 2) lds_f64x2(aS + 16 + 8 * c, u[c], u[c + 1]);
+    double nl[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
+      nl[q] = 0.0;
       if (!valid[q] || gi[q] <= j) continue;
-      const int li = q * PT + tid;
       if (own_p && gi[q] == pr) {
 #pragma unroll
         for (int c = 0; c < PNB; ++c) x[q][c] = lds_f64(bS + 8 * (c + 1));
       }
       double l = x[q][0];
       if (piv != 0.0) l = recip ? l * rinv : l / piv;
-      psm[jj * rhp + li] = l;
+      nl[q] = l;
+      psm[jj * rhp + q * PT + tid] = l;
+      x[q][0] = fma(-l, u[0], x[q][1]);  // next column first
+    }
+    // next column's candidate + warp reduction (overlaps the remaining updates)
+    bv = -1.0;
+    bi = INT_MAX;
 #pragma unroll
-      for (int c = 0; c < PNB - 1; ++c) x[q][c] = fma(-l, u[c], x[q][c + 1]);
+    for (int q = 0; q < RPT; ++q)
+      if (valid[q] && gi[q] > j) {
+        const double v = fabs(x[q][0]);
+        if (v > bv || (v == bv && gi[q] < bi)) { bv = v; bi = gi[q]; bq = q; }
+      }
+    {
+      double wv = bv;
+      int wi = bi;
+      warp_argmax_fast(wv, wi);
+      if (lane == 0) { wval[par ^ 1][warp] = wv; widx[par ^ 1][warp] = wi; }
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (!valid[q] || gi[q] <= j) continue;
+#pragma unroll
+      for (int c = 1; c < PNB - 1; ++c) x[q][c] = fma(-nl[q], u[c], x[q][c + 1]);
       x[q][PNB - 1] = 0.0;
     }
     PPROF(5);
+    __syncthreads();   // warp slots of the next column complete; rows j/p settled
   }
-  __syncthreads();
 
   // write back; publish the interchange map for the rowpanel kernel
   for (int e = tid; e < nb * myrows; e += PT) {
@@ -512,9 +545,8 @@ void panel_profile_read(unsigned long long* out) {
 // ======================================================================
 cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
                           unsigned long long* scale_bits, cudaStream_t s) {
-  const long long total = (long long)a.n * a.n;
-  int blocks = (int)((total + 255) / 256);
-  blocks = blocks > 64 ? 64 : (blocks < 1 ? 1 : blocks);
+  int blocks = a.n < 1024 ? a.n : 1024;
+  if (count > 16) blocks = (blocks + 15) / 16;
   count_launch();
   maxabs_kernel<<<dim3(blocks, count), 256, 0, s>>>(a, slots, scale_bits);
   return cudaGetLastError();

@@ -30,53 +30,69 @@ constexpr int THREADS = 256;
 constexpr int STAGE_BYTES = StageGeom<T, BN>::BYTES;  // 12 KB
 constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
 constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T * LDD * 8 + BN * LDR * 8 + 1024 + 256;
+constexpr int LDB = T + 4;         // prefetched B_i tile stride ([n][k])
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256;
+
+BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+BRI_DEVI void cp_async_commit_wait() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 
 // --------------------------------------------------------------- dinv
 // Invert the T x T diagonal blocks of the factor in slot F: unit lower (L) or
-// non-unit upper (U).  Outside [0, n) the block is the identity.
+// non-unit upper (U).  Outside [0, n) the block is the identity.  One CTA of
+// 256 threads per block: substitution over the T steps with the T x T
+// right-hand sides (the identity) spread over the threads.
 // dinv layout per item: [nblk][T x T column-major].
+constexpr int DINV_THREADS = 256;
+
 template <bool LOWER>
-__global__ void __launch_bounds__(T) dinv_kernel(ArenaView a, const int* fslots, double* dinv, int nblk, int blk0) {
+__global__ void __launch_bounds__(DINV_THREADS) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
+                                                            int nblk, int blk0) {
   extern __shared__ double dsm[];
-  double (*S)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm);            // S[c][r] = block(r, c)
-  double (*X)[T + 1] = reinterpret_cast<double (*)[T + 1]>(dsm + T * (T + 1));  // X[c][r] = inverse(r, c)
+  double* S = dsm;                 // S[c * (T+1) + r] = block(r, c)
+  double* X = dsm + T * (T + 1);   // X[c * (T+1) + r] = inverse(r, c)
   const int blk = blk0 + blockIdx.x, item = blockIdx.y;
   const double* F = a.base + (long long)fslots[item] * a.slot_elems;
   const int base = blk * T;
-  const int c = threadIdx.x;
-  for (int r = 0; r < T; ++r) {
+  for (int e = threadIdx.x; e < T * T; e += DINV_THREADS) {
+    const int r = e % T, c = e / T;
     const int gi = base + r, gj = base + c;
     double v = (gi < a.n && gj < a.n) ? F[gi + (long long)gj * a.ld] : (r == c ? 1.0 : 0.0);
     if (LOWER && r == c) v = 1.0;
     if (LOWER && r < c) v = 0.0;
     if (!LOWER && r > c) v = 0.0;
-    S[c][r] = v;
+    S[c * (T + 1) + r] = v;
+    X[c * (T + 1) + r] = (r == c) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // thread c solves T * x = e_c
-  double* x = X[c];
+  // thread layout: column c = tid % T, row group g = tid / T (4 groups of 16 rows)
+  const int c = threadIdx.x % T, g = threadIdx.x / T;
   if (LOWER) {
-    for (int r = 0; r < T; ++r) x[r] = 0.0;
-    x[c] = 1.0;
-    for (int r = c + 1; r < T; ++r) {
-      double s = 0.0;
-      for (int k = c; k < r; ++k) s = fma(S[k][r], x[k], s);
-      x[r] = -s;
+    for (int k = 0; k < T - 1; ++k) {
+      const double xk = X[c * (T + 1) + k];
+      for (int r = k + 1 + g; r < T; r += DINV_THREADS / T)
+        X[c * (T + 1) + r] = fma(-S[k * (T + 1) + r], xk, X[c * (T + 1) + r]);
+      __syncthreads();
     }
   } else {
-    for (int r = 0; r < T; ++r) x[r] = 0.0;
-    for (int r = c; r >= 0; --r) {
-      double s = (r == c) ? 1.0 : 0.0;
-      for (int k = r + 1; k <= c; ++k) s = fma(-S[k][r], x[k], s);
-      x[r] = s / S[r][r];
+    for (int k = T - 1; k >= 0; --k) {
+      if (g == 0) X[c * (T + 1) + k] /= S[k * (T + 1) + k];
+      __syncthreads();
+      const double xk = X[c * (T + 1) + k];
+      for (int r = g; r < k; r += DINV_THREADS / T)
+        X[c * (T + 1) + r] = fma(-S[k * (T + 1) + r], xk, X[c * (T + 1) + r]);
+      __syncthreads();
     }
   }
-  __syncthreads();
   double* out = dinv + ((long long)item * nblk + blk) * T * T;
-  for (int e = threadIdx.x; e < T * T; e += T) {
+  for (int e = threadIdx.x; e < T * T; e += DINV_THREADS) {
     const int r = e % T, cc = e / T;
-    out[e] = X[cc][r];
+    out[e] = X[cc * (T + 1) + r];
   }
 }
 
@@ -98,7 +114,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double* D = reinterpret_cast<double*>(smem + STAGES * STAGE_BYTES);   // Tinv_ii, [k][m] col-major (LDD)
   double* R = D + T * LDD;                                              // B_i - acc, [n][k] (LDR)
-  uint64_t* full = reinterpret_cast<uint64_t*>(R + BN * LDR);
+  double* Bst = R + BN * LDR;                                           // prefetched B_i, [n][k] (LDB)
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bst + BN * LDB);
   uint64_t* empty = full + STAGES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -143,6 +160,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     if (producer)
       for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt);
+    // prefetch Tinv_ii and B_i with cp.async; they land while the K loop runs
+    {
+      const double* Di = dinv + (long long)(row0 / T) * T * T;
+      for (int e = threadIdx.x; e < T * T / 2; e += THREADS) {
+        const int k = e / (T / 2), r2 = (e % (T / 2)) * 2;
+        cp_async16(&D[k * LDD + r2], Di + k * T + r2, true);
+      }
+      for (int e = threadIdx.x; e < BN * T / 2; e += THREADS) {
+        const int cc = e / (T / 2), r2 = (e % (T / 2)) * 2;
+        const bool ok = r2 < rows && c0 + cc < cend;
+        const double* src = ok ? W + (long long)(row0 + r2) + (long long)(c0 + cc) * p.ld : W;
+        cp_async16(&Bst[cc * LDB + r2], src, ok);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     WarpAcc<1, 2> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
@@ -163,6 +195,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // (the epilogue's __syncthreads below ends every read of the ring before reuse)
     it += KT;
 
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
     // R = B_i - acc  (rows >= rows and columns >= nrhs are zero)
 #pragma unroll
     for (int j = 0; j < 2; ++j)
@@ -171,15 +205,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int r = wm0 + g + ((v >> 1) << 3);
         const int cc = wn0 + j * 8 + 2 * t + (v & 1);
         const bool ok = r < rows && c0 + cc < cend;
-        const double bval = ok ? W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] : 0.0;
-        R[cc * LDR + r] = ok ? bval - acc.c[0][j][v] : 0.0;
+        R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - acc.c[0][j][v] : 0.0;
       }
-    // Tinv_ii into smem
-    const double* Di = dinv + (long long)(row0 / T) * T * T;
-    for (int e = threadIdx.x; e < T * T; e += THREADS) {
-      const int r = e % T, k = e / T;
-      D[k * LDD + r] = Di[e];
-    }
     __syncthreads();
     // X_i = Tinv_ii * R   (64 x 32 x 64 DMMA from smem)
     double x[2][4];
@@ -231,9 +258,9 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
   dim3 grid(nblocks, count);
   count_launch();
   if (lower)
-    dinv_kernel<true><<<grid, T, smem, s>>>(a, fslots, dinv, nblk, blk0);
+    dinv_kernel<true><<<grid, DINV_THREADS, smem, s>>>(a, fslots, dinv, nblk, blk0);
   else
-    dinv_kernel<false><<<grid, T, smem, s>>>(a, fslots, dinv, nblk, blk0);
+    dinv_kernel<false><<<grid, DINV_THREADS, smem, s>>>(a, fslots, dinv, nblk, blk0);
   return cudaGetLastError();
 }
 

@@ -110,6 +110,10 @@ class RunInfo:
     peak_blocks: int = 0
 
 
+class _TooBig(Exception):
+    """The schedule's resident working set does not fit the arena budget."""
+
+
 def _budget_slots(ws: Workspace, b: int, device: int) -> int:
     torch = _torch()
     block_bytes = b * padded_ld(b) * 8
@@ -117,7 +121,8 @@ def _budget_slots(ws: Workspace, b: int, device: int) -> int:
         budget = ws.arena_bytes
     else:
         free, _ = torch.cuda.mem_get_info(device)
-        budget = int(free * 0.85)
+        cached = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+        budget = int((free + cached) * 0.85)
     return max(1, budget // block_bytes)
 
 
@@ -134,9 +139,8 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
     max_slots = _budget_slots(ws, b, device)
     base_need = len(used) + live_values
     if base_need + 3 > max_slots:
-        raise BadPartitionError(
-            f"DAG needs {base_need} resident blocks of order {b} but the arena budget holds {max_slots}; "
-            "raise Workspace(arena_bytes=...) or use schedule='tree'")
+        raise _TooBig(f"DAG needs {base_need} resident blocks of order {b} but the arena budget holds "
+                      f"{max_slots}; raise Workspace(arena_bytes=...) or use schedule='tree'")
     chunk = max(1, min(width, (max_slots - base_need) // 2, 65535))
     nslots = min(max_slots, base_need + 2 * chunk + 1)
     info = RunInfo("dag", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),
@@ -290,20 +294,50 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
     return results, info
 
 
+def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots):
+    """DAG run over all roots; if the union does not fit the arena, split the
+    roots into halves (shared nodes are recomputed, memory stays bounded).
+    Groups run in root order, so the first error raised is the reference's."""
+    sched = build_from_specs(k, specs, paths0)
+    try:
+        tensors, info = _run_dag(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
+        return tensors, info, [sched]
+    except _TooBig as e:
+        if len(specs) == 1:
+            raise BadPartitionError(str(e)) from None
+    h = len(specs) // 2
+    p0 = paths0[:h] if paths0 is not None else None
+    p1 = paths0[h:] if paths0 is not None else None
+    t0, i0, s0 = _run_grouped(src, k, specs[:h], p0, ws, device, trace, invert_roots)
+    t1, i1, s1 = _run_grouped(src, k, specs[h:], p1, ws, device, trace, invert_roots)
+    i0.dag_nodes += i1.dag_nodes
+    i0.tree_nodes += i1.tree_nodes
+    i0.targets += i1.targets
+    i0.arena_slots = max(i0.arena_slots, i1.arena_slots)
+    return t0 + t1, i0, s0 + s1
+
+
 def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, invert_roots=True,
              paths0=None):
     device = ws.device if ws.device is not None else current_device()
     src, base, mr, mc = _source_for(provider, device)
     k = base.layout.k
     specs = specs_fn(mr, mc)
-    sched = build_from_specs(k, specs, paths0)
-    run = _run_tree if ws.schedule == "tree" else _run_dag
-    tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
+    if ws.schedule == "tree":
+        sched = build_from_specs(k, specs, paths0)
+        tensors, info = _run_tree(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
+        scheds = [sched]
+    else:
+        tensors, info, scheds = _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots)
+    executed_nodes = sum(len(s.nodes) for s in scheds)
+    sched = scheds[0]
+    if len(scheds) > 1:
+        sched = build_from_specs(k, specs, paths0)
     # reference accounting (tree semantics), per root
     for t in range(len(sched.specs)):
         ws.counters.add_nodes(sched.tree_nodes(t), targets=1 if invert_roots else 0)
     if ws.schedule == "dag":
-        ws.executed.add_nodes(len(sched.nodes), targets=len(sched.specs) if invert_roots else 0)
+        ws.executed.add_nodes(executed_nodes, targets=len(sched.specs) if invert_roots else 0)
     elif invert_roots:
         ws.executed.block_inversions += len(sched.specs)
     return tensors, info

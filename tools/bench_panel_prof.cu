@@ -24,7 +24,7 @@ int main() {
     cudaDeviceSynchronize();
     panel_profile_read(ph);
     printf("H=%d cycles/col:", n - j0);
-    const char* nm[6] = {"cand+warpargmax", "wrow copy", "syncthreads", "cta/cluster", "swap", "u+update"};
+    const char* nm[6] = {"ctawinner", "publish", "wait", "select", "swap", "update+nextcand"};
     for (int k = 0; k < 6; ++k) printf(" %s=%.0f", nm[k], ph[k] / 320.0);
     printf("  err=%s\n", cudaGetErrorString(cudaGetLastError()));
   }
