@@ -107,14 +107,6 @@ def dist_env():
     return rank, world, local
 
 
-def shard(targets, rank, world):
-    """Contiguous row-major chunks of targets per rank; a single target is replicated."""
-    if len(targets) == 1:
-        return list(targets), "weak"
-    per = (len(targets) + world - 1) // world
-    return targets[rank * per:(rank + 1) * per], "strong"
-
-
 def cpu_oracle_step(a, k, targets):
     from oracle import bri_oracle as orc
 
@@ -199,7 +191,9 @@ def run_ours(args):
     cfg = workloads.config(args.config, args.b)
     k, b = cfg["k"], cfg["b"]
     a = workloads.make_matrix(args.config, args.b)
-    my_targets, scaling = shard(cfg["targets"], rank, world)
+    from paper_1612_00001_b200.distributed import gather_blocks, shard_targets
+
+    my_targets, scaling = shard_targets(cfg["targets"], rank, world)
     sched = build_schedule(k, my_targets)
     flops_rank = workloads.run_flops(b, len(sched.nodes), len(my_targets))
 
@@ -246,12 +240,7 @@ def run_ours(args):
 
     # ---- gather results to rank 0 (strong scaling: the full inverse lands on rank 0)
     if dist is not None and scaling == "strong":
-        blocks = torch.stack(out) if out else torch.empty((0, b, b), dtype=torch.float64, device="cuda")
-        per = (len(cfg["targets"]) + world - 1) // world
-        pad = torch.zeros((per, b, b), dtype=torch.float64, device="cuda")
-        pad[: blocks.shape[0]] = blocks
-        gathered = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
-        dist.gather(pad, gathered, dst=0)
+        gather_blocks(out, cfg["targets"], rank, world, b)
 
     # ---- end-to-end through the public API from pinned host memory
     a_pin = torch.from_numpy(a).pin_memory()
