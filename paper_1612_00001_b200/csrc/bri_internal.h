@@ -59,6 +59,10 @@ cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStr
 cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, const int* pi,
                             int pi_stride, bool identity_src, cudaStream_t s);
 cudaError_t launch_pi_init(int* pi, int n, int count, cudaStream_t s);
+// dst X-column pi[x] = src X-column x (column scatter; X-columns are memory rows); pairs (src, dst)
+cudaError_t launch_colscatter(const ArenaView& a, const int* pairs, int count, const int* pi, int pi_stride,
+                              cudaStream_t s);
+cudaError_t launch_identity(const ArenaView& a, const int* slots, int slot_stride, int count, cudaStream_t s);
 int panel_width(int n);
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                          const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
@@ -66,7 +70,8 @@ cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int
                             int cbeg, int cend, const LuScratch& sc, int n_stride, int pair_stride,
                             cudaStream_t s);
 cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
-                         int npan, const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
+                         int npan, int a0, int a1, int b0, int b1, const LuScratch& sc, int n_stride,
+                         int pair_stride, cudaStream_t s);
 cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
                               const unsigned long long* scale_bits, int* status, cudaStream_t s);
 
@@ -75,7 +80,7 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
                         int blk0, int nblocks, cudaStream_t s);
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
                               const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int c_off, int nrhs, cudaStream_t s);
+                              int c_off, int nrhs, bool tri_rhs, cudaStream_t s);
 
 // Fused one-CTA node / inverse for n <= SMALL_MAX.
 // items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.

@@ -34,7 +34,11 @@ namespace bri {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = TILE_BK, STAGES = 4;
-constexpr int NUM_WARPS = 8;
+// 16 warps in a 4 x 4 grid, 32 x 32 warp tiles: four warps per scheduler hide
+// DMMA / LDS latency (8 warps of 64 x 32 tiles left the DMMA pipe ~80% busy).
+constexpr int WARPS_M = 4, WARPS_N = 4;
+constexpr int NUM_WARPS = WARPS_M * WARPS_N;
+constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
 constexpr int THREADS = NUM_WARPS * 32;
 constexpr int STAGE_BYTES = StageGeom<BM, BN>::BYTES;    // 32 KB
 constexpr int LDT = BM + 4;                              // epilogue tile stride (doubles)
@@ -83,9 +87,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt);
   }
 
-  const int wm0 = (warp & 1) * 64;   // 2 warps along M
-  const int wn0 = (warp >> 1) * 32;  // 4 warps along N
-  WarpAcc<4, 4> acc;
+  const int wm0 = (warp % WARPS_M) * WTM;
+  const int wn0 = (warp / WARPS_M) * WTN;
+  WarpAcc<WTM / 16, WTN / 8> acc;
   acc.zero();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;

@@ -81,6 +81,25 @@ __global__ void permcopy_kernel(ArenaView a, const int* pairs, const int* pi, in
     }
 }
 
+// X-column x of src -> X-column pi[x] of dst (memory rows, coalesced)
+__global__ void colscatter_kernel(ArenaView a, const int* pairs, const int* pi, int pi_stride) {
+  const int item = blockIdx.y;
+  const double* src = a.base + (long long)pairs[2 * item] * a.slot_elems;
+  double* dst = a.base + (long long)pairs[2 * item + 1] * a.slot_elems;
+  const int* p = pi + (long long)item * pi_stride;
+  for (int x = blockIdx.x; x < a.n; x += gridDim.x) {
+    const double* s = src + (long long)x * a.ld;
+    double* d = dst + (long long)p[x] * a.ld;
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) d[i] = s[i];
+  }
+}
+
+__global__ void identity_kernel(ArenaView a, const int* slots, int slot_stride) {
+  double* x = a.base + (long long)slots[slot_stride * blockIdx.y] * a.slot_elems;
+  for (int j = blockIdx.x; j < a.n; j += gridDim.x)
+    for (int i = threadIdx.x; i < a.n; i += blockDim.x) x[i + (long long)j * a.ld] = (i == j) ? 1.0 : 0.0;
+}
+
 __global__ void pi_init_kernel(int* pi, int n) {
   const int item = blockIdx.y;
   for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
@@ -486,6 +505,7 @@ struct LaswpArgs {
   ArenaView a;
   const int* slots;
   int J0, W, nbi, pidx0, npan;
+  int a0, a1, b0, b1;   // X-columns handled: [a0, a1) then [b0, b1)
   const int* sigma;
   const int* pairs;
   int n_stride, pair_stride;
@@ -496,8 +516,9 @@ __global__ void __launch_bounds__(RP_THREADS) laswp_kernel(LaswpArgs p) {
   const int n = p.a.n, ld = p.a.ld;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * (RP_THREADS / 32) + warp;
-  const int cc = c < p.J0 ? c : c + p.W;
-  if (cc >= n) return;
+  const int na = p.a1 - p.a0;
+  const int cc = c < na ? p.a0 + c : p.b0 + (c - na);
+  if (c >= na && cc >= p.b1) return;
   double* col = p.a.base + (long long)p.slots[item] * p.a.slot_elems + (long long)cc * ld;
   const int* sig = p.sigma + (long long)item * p.n_stride;
   for (int q = 0; q < p.npan; ++q) {
@@ -564,6 +585,21 @@ cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, con
   const int gx = a.n < 512 ? a.n : 512;
   count_launch();
   permcopy_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs, pi, pi_stride, identity_src ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colscatter(const ArenaView& a, const int* pairs, int count, const int* pi, int pi_stride,
+                              cudaStream_t s) {
+  const int gx = a.n < 1024 ? a.n : 1024;
+  count_launch();
+  colscatter_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs, pi, pi_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_identity(const ArenaView& a, const int* slots, int slot_stride, int count, cudaStream_t s) {
+  const int gx = a.n < 1024 ? a.n : 1024;
+  count_launch();
+  identity_kernel<<<dim3(gx, count), 256, 0, s>>>(a, slots, slot_stride);
   return cudaGetLastError();
 }
 
@@ -653,10 +689,17 @@ cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int
 }
 
 cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
-                        int npan, const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
-  const int cols = a.n - W;
+                        int npan, int a0, int a1, int b0, int b1, const LuScratch& sc, int n_stride,
+                        int pair_stride, cudaStream_t s) {
+  a1 = a1 > a0 ? a1 : a0;
+  b1 = b1 > b0 ? b1 : b0;
+  const int cols = (a1 - a0) + (b1 - b0);
   if (cols <= 0) return cudaSuccess;
   LaswpArgs p;
+  p.a0 = a0;
+  p.a1 = a1;
+  p.b0 = b0;
+  p.b1 = b1;
   p.a = a;
   p.slots = slots;
   p.J0 = J0;

@@ -44,56 +44,53 @@ BRI_DEVI void cp_async_commit_wait() {
 
 // --------------------------------------------------------------- dinv
 // Invert the T x T diagonal blocks of the factor in slot F: unit lower (L) or
-// non-unit upper (U).  Outside [0, n) the block is the identity.  One CTA of
-// 256 threads per block: substitution over the T steps with the T x T
-// right-hand sides (the identity) spread over the threads.
+// non-unit upper (U).  Outside [0, n) the block is the identity.  One warp per
+// column of the inverse (lane l owns rows l and l + 32), substitution by
+// shuffles: no block-wide barriers on the dependency chain.
 // dinv layout per item: [nblk][T x T column-major].
-constexpr int DINV_THREADS = 256;
+constexpr int DINV_WARPS = 8;
 
 template <bool LOWER>
-__global__ void __launch_bounds__(DINV_THREADS) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
-                                                            int nblk, int blk0) {
-  extern __shared__ double dsm[];
-  double* S = dsm;                 // S[c * (T+1) + r] = block(r, c)
-  double* X = dsm + T * (T + 1);   // X[c * (T+1) + r] = inverse(r, c)
-  const int blk = blk0 + blockIdx.x, item = blockIdx.y;
+__global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
+                                                               int nblk, int blk0) {
+  __shared__ double S[T][T + 1];   // S[c][r] = block(r, c)
+  const int cols_per_cta = DINV_WARPS;
+  const int blk = blk0 + blockIdx.x / (T / cols_per_cta), item = blockIdx.y;
+  const int c = (blockIdx.x % (T / cols_per_cta)) * cols_per_cta + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   const double* F = a.base + (long long)fslots[item] * a.slot_elems;
   const int base = blk * T;
-  for (int e = threadIdx.x; e < T * T; e += DINV_THREADS) {
-    const int r = e % T, c = e / T;
-    const int gi = base + r, gj = base + c;
-    double v = (gi < a.n && gj < a.n) ? F[gi + (long long)gj * a.ld] : (r == c ? 1.0 : 0.0);
-    if (LOWER && r == c) v = 1.0;
-    if (LOWER && r < c) v = 0.0;
-    if (!LOWER && r > c) v = 0.0;
-    S[c * (T + 1) + r] = v;
-    X[c * (T + 1) + r] = (r == c) ? 1.0 : 0.0;
+  for (int e = threadIdx.x; e < T * T; e += DINV_WARPS * 32) {
+    const int r = e % T, cc = e / T;
+    const int gi = base + r, gj = base + cc;
+    double v = (gi < a.n && gj < a.n) ? F[gi + (long long)gj * a.ld] : (r == cc ? 1.0 : 0.0);
+    if (LOWER && r == cc) v = 1.0;
+    if (LOWER && r < cc) v = 0.0;
+    if (!LOWER && r > cc) v = 0.0;
+    S[cc][r] = v;
   }
   __syncthreads();
-  // thread layout: column c = tid % T, row group g = tid / T (4 groups of 16 rows)
-  const int c = threadIdx.x % T, g = threadIdx.x / T;
+  double x0 = (lane == c) ? 1.0 : 0.0, x1 = (lane + 32 == c) ? 1.0 : 0.0;  // rows lane, lane + 32
   if (LOWER) {
+#pragma unroll 4
     for (int k = 0; k < T - 1; ++k) {
-      const double xk = X[c * (T + 1) + k];
-      for (int r = k + 1 + g; r < T; r += DINV_THREADS / T)
-        X[c * (T + 1) + r] = fma(-S[k * (T + 1) + r], xk, X[c * (T + 1) + r]);
-      __syncthreads();
+      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+      if (lane > k) x0 = fma(-S[k][lane], xk, x0);
+      if (lane + 32 > k) x1 = fma(-S[k][lane + 32], xk, x1);
     }
   } else {
+#pragma unroll 4
     for (int k = T - 1; k >= 0; --k) {
-      if (g == 0) X[c * (T + 1) + k] /= S[k * (T + 1) + k];
-      __syncthreads();
-      const double xk = X[c * (T + 1) + k];
-      for (int r = g; r < k; r += DINV_THREADS / T)
-        X[c * (T + 1) + r] = fma(-S[k * (T + 1) + r], xk, X[c * (T + 1) + r]);
-      __syncthreads();
+      const double dk = S[k][k];
+      if (k >= 32) { if (lane == k - 32) x1 /= dk; } else { if (lane == k) x0 /= dk; }
+      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+      if (lane < k) x0 = fma(-S[k][lane], xk, x0);
+      if (lane + 32 < k) x1 = fma(-S[k][lane + 32], xk, x1);
     }
   }
-  double* out = dinv + ((long long)item * nblk + blk) * T * T;
-  for (int e = threadIdx.x; e < T * T; e += DINV_THREADS) {
-    const int r = e % T, cc = e / T;
-    out[e] = X[cc * (T + 1) + r];
-  }
+  double* out = dinv + ((long long)item * nblk + blk) * T * T + (long long)c * T;
+  out[lane] = x0;
+  out[lane + 32] = x1;
 }
 
 // --------------------------------------------------------------- solve
@@ -105,6 +102,8 @@ struct TrsmArgs {
   const double* dinv;   // per item [nblk][T*T]
   int nblk;
   int r0, nr, c_off, nrhs;
+  int tri_rhs;          // LOWER only: right-hand side is unit-lower-triangular (an identity
+                        // being inverted): rows above a column's diagonal are zero and stay zero
 };
 
 template <bool LOWER>
@@ -145,11 +144,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   int it = 0;  // k-tiles consumed so far (ring position / phase)
-  for (int ii = 0; ii < nb; ++ii) {
+  // first block row with nonzeros in this CTA's columns (triangular right-hand side)
+  const int i0 = (LOWER && p.tri_rhs) ? max(0, (c0 - p.r0) / T) : 0;
+  for (int ii = LOWER ? i0 : 0; ii < nb; ++ii) {
     const int i = LOWER ? ii : nb - 1 - ii;
     const int row0 = p.r0 + i * T;
     const int rows = min(T, p.r0 + p.nr - row0);
-    const int klo = LOWER ? p.r0 : row0 + T;
+    const int klo = LOWER ? p.r0 + i0 * T : row0 + T;
     const int khi = LOWER ? row0 : p.r0 + p.nr;
     const int K = khi - klo;
     const int KT = K > 0 ? (K + TILE_BK - 1) / TILE_BK : 0;
@@ -246,27 +247,18 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
                         int blk0, int nblocks, cudaStream_t s) {
   const int nblk = (a.n + T - 1) / T;
   if (nblocks <= 0) nblocks = nblk - blk0;
-  const int smem = 2 * T * (T + 1) * 8;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(dinv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(dinv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  dim3 grid(nblocks, count);
+  dim3 grid(nblocks * (T / DINV_WARPS), count);
   count_launch();
   if (lower)
-    dinv_kernel<true><<<grid, DINV_THREADS, smem, s>>>(a, fslots, dinv, nblk, blk0);
+    dinv_kernel<true><<<grid, DINV_WARPS * 32, 0, s>>>(a, fslots, dinv, nblk, blk0);
   else
-    dinv_kernel<false><<<grid, DINV_THREADS, smem, s>>>(a, fslots, dinv, nblk, blk0);
+    dinv_kernel<false><<<grid, DINV_WARPS * 32, 0, s>>>(a, fslots, dinv, nblk, blk0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
                               const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int c_off, int nrhs, cudaStream_t s) {
+                              int c_off, int nrhs, bool tri_rhs, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -286,6 +278,7 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
   p.nr = nr;
   p.c_off = c_off;
   p.nrhs = nrhs;
+  p.tri_rhs = tri_rhs ? 1 : 0;
   dim3 grid((nrhs + BN - 1) / BN, count);
   count_launch();
   if (lower)
