@@ -80,6 +80,7 @@ struct DevBuf {
 struct GraphEntry {
   std::vector<uintptr_t> key;
   cudaGraphExec_t exec;
+  long long kernels;  // kernel nodes: counted as launches on every replay
 };
 
 struct bri_ctx {
@@ -350,6 +351,7 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
     if (e.key == key) hit = &e;
   if (hit != nullptr) {
     BRI_CHECK(cudaGraphLaunch(hit->exec, g));
+    bri::g_launches.fetch_add(hit->kernels, std::memory_order_relaxed);
   } else {
     bool seen = false;
     for (auto& k : ctx->seen)
@@ -367,6 +369,17 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
         return rc;
       }
       if (e != cudaSuccess) return fail("cudaStreamEndCapture", e);
+      size_t nnodes = 0;
+      BRI_CHECK(cudaGraphGetNodes(graph, nullptr, &nnodes));
+      std::vector<cudaGraphNode_t> nodes(nnodes);
+      long long kernels = 0;
+      if (nnodes) {
+        BRI_CHECK(cudaGraphGetNodes(graph, nodes.data(), &nnodes));
+        for (auto nd : nodes) {
+          cudaGraphNodeType ty;
+          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++kernels;
+        }
+      }
       cudaGraphExec_t exec = nullptr;
       const cudaError_t e2 = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
@@ -375,8 +388,9 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
         cudaGraphExecDestroy(ctx->graphs.front().exec);
         ctx->graphs.erase(ctx->graphs.begin());
       }
-      ctx->graphs.push_back({key, exec});
+      ctx->graphs.push_back({key, exec, kernels});
       BRI_CHECK(cudaGraphLaunch(exec, g));
+      // the captured launches went through count_launch() during capture
     }
   }
   BRI_CHECK(cudaEventRecord(ctx->ev_out, g));

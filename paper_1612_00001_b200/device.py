@@ -87,6 +87,12 @@ class Arena:
         for s in list(self._live):
             self.release(s)
 
+    def reset(self, gauge=None) -> None:
+        """Reuse for a new run: every slot free, accounting to `gauge`."""
+        self.release_all()
+        self.gauge = gauge
+        self._free = list(range(self.nslots - 1, -1, -1))
+
     @property
     def live(self) -> int:
         return len(self._live)
@@ -171,6 +177,39 @@ class Arena:
                 self.handle = None
         except Exception:
             pass
+
+
+_CACHE: dict = {}
+
+
+def cached_arena(n: int, nslots: int, device: int, gauge=None) -> Arena:
+    """One reusable arena per device: repeated runs of the same geometry keep the
+    same device addresses (so their CUDA graphs replay) and skip reallocation."""
+    ar = _CACHE.get(device)
+    if ar is not None and ar.handle is not None and ar.n == n and ar.nslots >= nslots:
+        ar.reset(gauge)
+        return ar
+    if ar is not None:
+        ar.close()
+        _CACHE.pop(device, None)
+    ar = Arena(n, nslots, device=device, gauge=gauge)
+    _CACHE[device] = ar
+    return ar
+
+
+def cached_bytes(device: int, n: int) -> int:
+    """Device bytes held by the cached arena that a run of order n could reuse."""
+    ar = _CACHE.get(device)
+    if ar is None or ar.handle is None:
+        return 0
+    return ar.nslots * ar.n * ar.ld * 8
+
+
+def release_cached_memory() -> None:
+    """Free the cached arenas (their memory returns to PyTorch's allocator)."""
+    for ar in list(_CACHE.values()):
+        ar.close()
+    _CACHE.clear()
 
 
 def fp64_peak_tflops(iters: int = 4096) -> float:

@@ -37,7 +37,7 @@ import numpy as np
 
 from .core import Block, Workspace
 from .dag import build_from_specs, build_schedule, target_maps
-from .device import Arena, current_device, padded_ld
+from .device import Arena, cached_arena, cached_bytes, current_device, padded_ld
 from .errors import (BadPartitionError, DimensionMismatchError, IndexOutOfRangeError,
                      SingularBlockError, SingularPivotError)
 from .frames import PLAN, Frame, Quadrant, root_frame, split_frame
@@ -122,7 +122,7 @@ def _budget_slots(ws: Workspace, b: int, device: int) -> int:
     else:
         free, _ = torch.cuda.mem_get_info(device)
         cached = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
-        budget = int((free + cached) * 0.85)
+        budget = int((free + cached + cached_bytes(device, b)) * 0.85)
     return max(1, budget // block_bytes)
 
 
@@ -148,7 +148,8 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
     status = torch.zeros(max(1, len(sched.nodes)), dtype=torch.int32, device=f"cuda:{device}")
     root_status = torch.zeros(max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
     results = []
-    with Arena(b, nslots, device=device, gauge=ws.gauge) as arena:
+    arena = cached_arena(b, nslots, device, gauge=ws.gauge)
+    try:
         mslot = {}
         for ij in used:
             mslot[ij] = arena.alloc()
@@ -215,6 +216,8 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
             for t in range(nroots):
                 sched.walk(t, on_node=on_node)
         info.peak_blocks = ws.gauge.peak_blocks
+    finally:
+        arena.release_all()
     sched.first_failure(pstat, rstat, b)
     return results, info
 
@@ -233,7 +236,8 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
     # one permutation buffer per recursion depth: a node's pivot permutation must
     # survive the evaluation of its rt and l subtrees
     perms = [torch.zeros(b, dtype=torch.int32, device=dev) for _ in range(k + 1)]
-    with Arena(b, nslots, device=device, gauge=ws.gauge) as arena:
+    arena = cached_arena(b, nslots, device, gauge=ws.gauge)
+    try:
         for t, (frame0, mr, mc) in enumerate(sched.specs):
 
             def fetch(i, j):
@@ -291,6 +295,8 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
                 results.append(arena.view(root).clone())
                 arena.release(root)
         info.peak_blocks = ws.gauge.peak_blocks
+    finally:
+        arena.release_all()
     return results, info
 
 
