@@ -1,0 +1,137 @@
+"""Drop-in API surface on the device: primitives, schur_eliminate, reduce_frame, invert_full,
+workspace accounting and error behaviour (mirrors pkg/tests/test_core.py / test_engine.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import rng, shifted
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bri():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1612_00001_b200 as bri
+
+    return bri
+
+
+def test_primitives(bri):
+    ws = bri.Workspace()
+    x = ws.from_array([[1.0, 2.0], [3.0, 4.0]])
+    y = ws.from_array([[0.0, 1.0], [1.0, 0.0]])
+    np.testing.assert_array_equal(bri.multiply(x, y).data, [[2.0, 1.0], [4.0, 3.0]])
+    a = rng(11).standard_normal((128, 128))
+    b = rng(12).standard_normal((128, 128))
+    np.testing.assert_allclose(bri.multiply(ws.from_array(a), ws.from_array(b)).data, a @ b, rtol=0, atol=1e-12)
+    d = bri.subtract(ws.from_array([[4.0, 2.0], [1.0, 3.0]]), ws.from_array([[1.0, 1.0], [1.0, 1.0]]))
+    np.testing.assert_array_equal(d.data, [[3.0, 1.0], [0.0, 2.0]])
+    z = ws.from_array([[4.0, 2.0], [1.0, 3.0]])
+    assert bri.subtract(z, ws.identity(2), in_place=True) is z
+    np.testing.assert_array_equal(z.data, [[3.0, 2.0], [1.0, 2.0]])
+    inv = bri.invert_dense(ws.from_array([[4.0, 2.0], [1.0, 3.0]]))
+    np.testing.assert_allclose(inv.data, [[0.3, -0.2], [-0.1, 0.4]], atol=1e-15)
+    with pytest.raises(bri.SingularBlockError):
+        bri.invert_dense(ws.from_array([[1.0, 2.0], [2.0, 4.0]]))
+    with pytest.raises(bri.DimensionMismatchError):
+        bri.multiply(ws.zeros(2), ws.zeros(3))
+    assert ws.counters.block_multiplications == 2 and ws.counters.block_subtractions == 2
+    assert ws.counters.block_inversions == 1
+
+
+def test_lu_factor_matches_reference(bri, golden):
+    data, _ = golden
+    fac = bri.lu_factor(bri.Workspace().from_array(data["lu6_matrix"]))
+    np.testing.assert_array_equal(fac.pivots, data["lu6_pivots"])
+    np.testing.assert_allclose(fac.packed_lu, data["lu6_packed"], rtol=0, atol=1e-13)
+    with pytest.raises(bri.SingularBlockError) as exc:
+        bri.lu_factor(bri.Workspace().from_array([[1.0, 2.0], [2.0, 4.0]]))
+    assert exc.value.pivot_index == 2
+
+
+def test_invert_dense_known_answers(bri, golden):
+    data, _ = golden
+    h = 1.0 / (np.arange(4)[:, None] + np.arange(4)[None, :] + 1.0)
+    np.testing.assert_allclose(bri.invert_dense(bri.Workspace().from_array(h)).data, data["hilbert4_inv"],
+                               rtol=1e-9)
+    for n in (1, 5, 12, 33, 64, 100):
+        got = bri.invert_dense(bri.Workspace().from_array(data[f"inv{n}_matrix"])).data
+        ref = data[f"inv{n}_out"]
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n", [2, 100])
+def test_schur_eliminate(bri, n):
+    ws = bri.Workspace()
+    blocks = [shifted(n, 40 + i) for i in range(4)]
+    g = ((ws.from_array(blocks[0]), ws.from_array(blocks[1])), (ws.from_array(blocks[2]), ws.from_array(blocks[3])))
+    out = bri.schur_eliminate(g, bri.Quadrant.D)
+    a, b, c, d = blocks
+    want = a - b @ np.linalg.solve(d, c)
+    assert np.abs(out.data - want).max() <= 1e-11 * np.abs(want).max()
+    assert ws.gauge.live_blocks == 1  # inputs consumed
+    out.release()
+
+
+def test_reduce_frame_matches_dense_schur(bri):
+    a = shifted(5, 81)
+    prov = bri.make_memory_provider(a, 5)
+    out = bri.reduce_frame(prov, bri.root_frame(5))
+    want = a[0, 0] - a[0, 1:] @ np.linalg.inv(a[1:, 1:]) @ a[1:, 0]
+    assert out.data[0, 0] == pytest.approx(want, abs=1e-9)
+    k2 = bri.make_memory_provider(np.array([[4.0, 2.0], [1.0, 3.0]]), 2)
+    assert bri.reduce_frame(k2, bri.root_frame(2)).data[0, 0] == pytest.approx(10.0 / 3.0, abs=1e-15)
+
+
+def test_invert_full_summary_and_parity(bri):
+    from oracle import bri_oracle as orc
+
+    a = shifted(8 * 3, 89)
+    prov = bri.make_memory_provider(a, 4)
+    sink = bri.MemorySink(prov.layout)
+    s = bri.invert_full(prov, sink, jobs=2)
+    want = bri.predicted_counts(4)
+    assert s.counters.schur_nodes == 16 * want.schur_nodes
+    assert s.counters.block_inversions == 16 * want.block_inversions
+    assert (s.m, s.k, s.b, s.l) == (24, 4, 6, 0)
+    assert s.executed.schur_nodes == 116
+    assert s.peak_bytes == s.peak_blocks * 8 * 6 * 6 and s.wall_ms > 0
+    ref = orc.lu_invert_full(a)
+    assert np.abs(sink.finalize() - ref).max() <= 1e-8 * np.abs(ref).max()
+
+
+def test_errors_and_edges(bri):
+    prov = bri.make_memory_provider(np.eye(4), 2)
+    with pytest.raises(bri.IndexOutOfRangeError):
+        bri.invert_block(prov, 0, 1)
+    with pytest.raises(bri.IndexOutOfRangeError):
+        bri.invert_block(prov, 1, 3)
+    with pytest.raises(bri.BadPartitionError):
+        bri.make_memory_provider(shifted(10, 1), 4)  # padded layouts: not on the device path yet
+    with pytest.raises(bri.SingularPivotError):  # exact I: off-diagonal pivots are singular
+        bri.invert_block(bri.make_memory_provider(np.eye(6), 3), 1, 2)
+    ws = bri.Workspace()
+    for al in range(1, 4):  # identity diagonal targets are exact
+        out = bri.invert_block(bri.make_memory_provider(np.eye(6), 3), al, al, ws)
+        np.testing.assert_array_equal(out.data, np.eye(2))
+        out.release()
+    assert ws.gauge.live_blocks == 0
+    nan = shifted(8, 3)
+    nan[0, 0] = np.nan
+    with pytest.raises((bri.SingularPivotError, bri.SingularBlockError)):
+        bri.invert_block(bri.make_memory_provider(nan, 2), 1, 1)
+
+
+def test_device_and_host_inputs_agree(bri):
+    import torch
+
+    a = shifted(256, 9)
+    host = bri.invert_block(bri.make_memory_provider(a, 2), 2, 1).data
+    dev = bri.invert_block(bri.make_memory_provider(torch.from_numpy(a).cuda(), 2), 2, 1).data
+    pin = bri.invert_block(bri.make_memory_provider(torch.from_numpy(a).pin_memory(), 2), 2, 1).data
+    np.testing.assert_array_equal(host, dev)
+    np.testing.assert_array_equal(host, pin)
