@@ -11,6 +11,13 @@ namespace bri {
 // Every kernel launch made by the library bumps this (exported as bri_launch_count).
 void count_launch();
 
+// One-time kernel attribute setup (dynamic shared memory), done at context creation
+// so that hot-path sequences can be captured into CUDA graphs on first use.
+cudaError_t configure_gemm();
+cudaError_t configure_lu();
+cudaError_t configure_small();
+cudaError_t configure_trsm();
+
 constexpr int NBMAX = 32;        // LU panel width upper bound
 constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
 constexpr int TRSM_BLOCK = 64;   // diagonal block of the fused triangular solve

@@ -353,13 +353,7 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
     BRI_CHECK(cudaGraphLaunch(hit->exec, g));
     bri::g_launches.fetch_add(hit->kernels, std::memory_order_relaxed);
   } else {
-    bool seen = false;
-    for (auto& k : ctx->seen)
-      if (k == key) seen = true;
-    if (!seen) {
-      ctx->seen.push_back(key);
-      rc = issue(g);
-    } else {
+    {
       BRI_CHECK(cudaStreamBeginCapture(g, cudaStreamCaptureModeThreadLocal));
       rc = issue(g);
       cudaGraph_t graph = nullptr;
@@ -479,6 +473,10 @@ int bri_ctx_create(int device, bri_ctx** out) {
   if (out == nullptr) return fail_msg("bri_ctx_create: null out");
   BRI_CHECK(cudaSetDevice(device));
   if (get_encoder() == nullptr) return fail_msg("cuTensorMapEncodeTiled unavailable (driver too old?)");
+  BRI_CHECK(configure_gemm());
+  BRI_CHECK(configure_lu());
+  BRI_CHECK(configure_small());
+  BRI_CHECK(configure_trsm());
   bri_ctx* c = new bri_ctx();
   c->device = device;
   int prio_low = 0, prio_high = 0;

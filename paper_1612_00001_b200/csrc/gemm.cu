@@ -148,14 +148,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 int gemm_smem_bytes() { return SMEM_BYTES; }
 
+cudaError_t configure_gemm() {
+  return cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+}
+
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p0,
                         int count, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   if (p0.M <= 0 || p0.N <= 0 || count <= 0) return cudaSuccess;
   GemmParams p = p0;
   p.tiles_m = (p.M + BM - 1) / BM;

@@ -179,16 +179,21 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   // 34-wide buffer whose tail is zero, so the update reads u[c] = buf[c + 2]
   // with aligned 16-byte loads.
   constexpr int SW = 34;
+  // one 544-byte message per row: L part, shifted live part, (value, row, origin)
+  struct __align__(16) RowMsg {
+    double L[PNB];
+    double S[SW];
+    double val;
+    int idx, orig;
+  };
+  static_assert(sizeof(RowMsg) % 16 == 0, "bulk copies move 16-byte multiples");
   extern __shared__ double psm[];                       // nb columns x rhp rows, then rhp ints
   __shared__ double wval[2][PW];
   __shared__ int widx[2][PW];
-  __shared__ __align__(16) double cL[2][MAXCS][PNB], cS[2][MAXCS][SW];   // candidates (per source CTA)
-  __shared__ double cval[2][MAXCS];
-  __shared__ int cidx[2][MAXCS], corig[2][MAXCS];
-  __shared__ __align__(16) double rL[2][PNB], rS[2][SW];                 // row j (from its owner CTA)
-  __shared__ int rorig[2];
-  __shared__ __align__(8) uint64_t xbar[2];                              // exchange mbarriers (cs > 1)
-  __shared__ __align__(16) double stS[2][SW], stJ[2][SW];               // local staging (cs > 1)
+  __shared__ RowMsg cmsg[2][MAXCS];                     // candidates, by source CTA rank
+  __shared__ RowMsg jmsg[2];                            // row j, from its owner CTA
+  __shared__ RowMsg cstg[2], jstg[2];                   // local staging of outgoing messages (cs > 1)
+  __shared__ __align__(8) uint64_t xbar[2];             // exchange mbarriers (cs > 1)
 
   const int cs = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
@@ -200,10 +205,14 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   const int row_lo = j0 + rank * p.rows_per_cta;
   const int myrows = max(0, min(n, row_lo + p.rows_per_cta) - row_lo);
   // bytes each CTA receives per column: cs candidates + row j
-  const uint32_t xbytes = (uint32_t)cs * (2 * PNB * 8 + 8 + 4 + 4) + (2 * PNB * 8 + 4);
+  const uint32_t xbytes = (uint32_t)(cs + 1) * (uint32_t)sizeof(RowMsg);
 
-  for (int e = tid; e < 2 * MAXCS * SW; e += PT) (&cS[0][0][0])[e] = 0.0;
-  for (int e = tid; e < 2 * SW; e += PT) (&rS[0][0])[e] = 0.0;
+  for (int e = tid; e < 2 * MAXCS * SW; e += PT) cmsg[e / (MAXCS * SW)][(e / SW) % MAXCS].S[e % SW] = 0.0;
+  for (int e = tid; e < 2 * SW; e += PT) {
+    jmsg[e / SW].S[e % SW] = 0.0;
+    cstg[e / SW].S[e % SW] = 0.0;
+    jstg[e / SW].S[e % SW] = 0.0;
+  }
   if (tid == 0) {
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
@@ -260,87 +269,84 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     uint32_t aL, aS, bL, bS;
     int pr, uorig, jorig;
     if (cs > 1) {
-      // every destination (incl. ourselves) receives our candidate in slot `rank`
+      // stage our CTA candidate (and row j if we own it) as one message each,
+      // then one lane bulk-copies it into slot `rank` of every CTA of the cluster
       if (have && warp == ((lw % PT) >> 5)) {
-        if (lane == (lw & 31)) store_live_row<RPT>(stS[par], x, lw / PT);
-        __syncwarp();
-        const double sv = stS[par][lane + 1];
-        const double lv = lane < jj ? psm[lane * rhp + lw] : 0.0;
-        const int ro = orig[lw];
-        for (int d = 0; d < cs; ++d) {
-          const uint32_t mb = dsmem_addr(&xbar[par], d);
-          st_async_f64(dsmem_addr(&cL[par][rank][lane], d), lv, mb);
-          st_async_f64(dsmem_addr(&cS[par][rank][lane + 1], d), sv, mb);
-          if (lane == 0) {
-            st_async_f64(dsmem_addr(&cval[par][rank], d), cv, mb);
-            st_async_s32(dsmem_addr(&cidx[par][rank], d), ci, mb);
-            st_async_s32(dsmem_addr(&corig[par][rank], d), ro, mb);
-          }
+        if (lane == (lw & 31)) {
+          store_live_row<RPT>(cstg[par].S, x, lw / PT);
+          cstg[par].val = cv;
+          cstg[par].idx = ci;
+          cstg[par].orig = orig[lw];
         }
+        cstg[par].L[lane] = lane < jj ? psm[lane * rhp + lw] : 0.0;
       } else if (!have && warp == 0) {
-        for (int d = 0; d < cs; ++d) {
-          const uint32_t mb = dsmem_addr(&xbar[par], d);
-          st_async_f64(dsmem_addr(&cL[par][rank][lane], d), 0.0, mb);
-          st_async_f64(dsmem_addr(&cS[par][rank][lane + 1], d), 0.0, mb);
-          if (lane == 0) {
-            st_async_f64(dsmem_addr(&cval[par][rank], d), -1.0, mb);
-            st_async_s32(dsmem_addr(&cidx[par][rank], d), INT_MAX, mb);
-            st_async_s32(dsmem_addr(&corig[par][rank], d), -1, mb);
-          }
+        cstg[par].L[lane] = 0.0;
+        if (lane == 0) {
+          cstg[par].val = -1.0;
+          cstg[par].idx = INT_MAX;
+          cstg[par].orig = -1;
         }
       }
       if (own_j && warp == ((lj % PT) >> 5)) {
-        if (lane == (lj & 31)) store_live_row<RPT>(stJ[par], x, lj / PT);
+        if (lane == (lj & 31)) {
+          store_live_row<RPT>(jstg[par].S, x, lj / PT);
+          jstg[par].orig = orig[lj];
+        }
+        jstg[par].L[lane] = lane < jj ? psm[lane * rhp + lj] : 0.0;
+      }
+      const bool pub_c = (have && warp == ((lw % PT) >> 5)) || (!have && warp == 0);
+      const bool pub_j = own_j && warp == ((lj % PT) >> 5);
+      if (pub_c || pub_j) {
+        fence_proxy_async_smem();   // generic smem writes -> visible to the bulk-copy engine
         __syncwarp();
-        const double sv = stJ[par][lane + 1];
-        const double lv = lane < jj ? psm[lane * rhp + lj] : 0.0;
-        const int ro = orig[lj];
-        for (int d = 0; d < cs; ++d) {
-          const uint32_t mb = dsmem_addr(&xbar[par], d);
-          st_async_f64(dsmem_addr(&rL[par][lane], d), lv, mb);
-          st_async_f64(dsmem_addr(&rS[par][lane + 1], d), sv, mb);
-          if (lane == 0) st_async_s32(dsmem_addr(&rorig[par], d), ro, mb);
+        if (lane == 0) {
+          for (int d = 0; d < cs; ++d) {
+            const uint32_t mb = dsmem_addr(&xbar[par], d);
+            if (pub_c) bulk_s2cluster(dsmem_addr(&cmsg[par][rank], d), &cstg[par], sizeof(RowMsg), mb);
+            if (pub_j) bulk_s2cluster(dsmem_addr(&jmsg[par], d), &jstg[par], sizeof(RowMsg), mb);
+          }
         }
       }
       PPROF(1);
       mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);
       PPROF(2);
-      double gv = lane < cs ? cval[par][lane] : -1.0;
-      int gidx = lane < cs ? cidx[par][lane] : INT_MAX;
+      double gv = lane < cs ? cmsg[par][lane].val : -1.0;
+      int gidx = lane < cs ? cmsg[par][lane].idx : INT_MAX;
+      const int myidx = gidx;
       warp_argmax_fast(gv, gidx);
-      const int gr = __ffs(__ballot_sync(0xffffffffu, lane < cs && gidx != INT_MAX && cidx[par][lane] == gidx)) - 1;
+      const int gr = __ffs(__ballot_sync(0xffffffffu, lane < cs && gidx != INT_MAX && myidx == gidx)) - 1;
       const bool none = gidx == INT_MAX;  // all NaN: idamax returns the first index
       pr = none ? j : gidx;
-      aL = none ? smem_u32(rL[par]) : smem_u32(cL[par][gr]);
-      aS = none ? smem_u32(rS[par]) : smem_u32(cS[par][gr]);
-      uorig = none ? rorig[par] : corig[par][gr];
-      jorig = rorig[par];
+      aL = none ? smem_u32(jmsg[par].L) : smem_u32(cmsg[par][gr].L);
+      aS = none ? smem_u32(jmsg[par].S) : smem_u32(cmsg[par][gr].S);
+      uorig = none ? jmsg[par].orig : cmsg[par][gr].orig;
+      jorig = jmsg[par].orig;
     } else {
       if (have && warp == ((lw % PT) >> 5)) {
         if (lane == (lw & 31)) {
-          store_live_row<RPT>(cS[par][0], x, lw / PT);
-          corig[par][0] = orig[lw];
+          store_live_row<RPT>(cmsg[par][0].S, x, lw / PT);
+          cmsg[par][0].orig = orig[lw];
         }
-        if (lane < jj) cL[par][0][lane] = psm[lane * rhp + lw];
+        if (lane < jj) cmsg[par][0].L[lane] = psm[lane * rhp + lw];
       }
       if (own_j && warp == ((lj % PT) >> 5)) {
         if (lane == (lj & 31)) {
-          store_live_row<RPT>(rS[par], x, lj / PT);
-          rorig[par] = orig[lj];
+          store_live_row<RPT>(jmsg[par].S, x, lj / PT);
+          jmsg[par].orig = orig[lj];
         }
-        if (lane < jj) rL[par][lane] = psm[lane * rhp + lj];
+        if (lane < jj) jmsg[par].L[lane] = psm[lane * rhp + lj];
       }
       PPROF(1);
       __syncthreads();
       PPROF(2);
       pr = have ? ci : j;
-      aL = have ? smem_u32(cL[par][0]) : smem_u32(rL[par]);
-      aS = have ? smem_u32(cS[par][0]) : smem_u32(rS[par]);
-      uorig = have ? corig[par][0] : rorig[par];
-      jorig = rorig[par];
+      aL = have ? smem_u32(cmsg[par][0].L) : smem_u32(jmsg[par].L);
+      aS = have ? smem_u32(cmsg[par][0].S) : smem_u32(jmsg[par].S);
+      uorig = have ? cmsg[par][0].orig : jmsg[par].orig;
+      jorig = jmsg[par].orig;
     }
-    bL = smem_u32(rL[par]);
-    bS = smem_u32(rS[par]);
+    bL = smem_u32(jmsg[par].L);
+    bS = smem_u32(jmsg[par].S);
     PPROF(3);
     // ---- (4) interchange, scale, rank-1 update; the next column's candidate
     //          is formed as soon as its values are updated
@@ -614,13 +620,6 @@ int panel_width(int n) { return n > 0 ? NBMAX : NBMAX; }
 
 template <int RPT>
 static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         160 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   const size_t smem = (size_t)p.nb * p.rhp * 8 + (size_t)p.rhp * 4 + 16;
   if (smem > 160 * 1024) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -637,6 +636,13 @@ static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s
   cfg.numAttrs = 1;
   count_launch();
   return cudaLaunchKernelEx(&cfg, lu_panel_kernel<RPT>, p);
+}
+
+cudaError_t configure_lu() {
+  cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  return e;
 }
 
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,

@@ -185,19 +185,23 @@ template <int NMAX>
 cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int mode, int* status,
                            cudaStream_t s) {
   const int smem = 3 * NMAX * (NMAX + 1) * 8;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(small_node_kernel<NMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   count_launch();
   small_node_kernel<NMAX><<<count, SN_THREADS, smem, s>>>(a, items, mode, status);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+cudaError_t configure_small() {
+  cudaError_t e = cudaFuncSetAttribute(small_node_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       3 * 32 * 33 * 8);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(small_node_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 65 * 8);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(small_node_kernel<SMALL_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             3 * SMALL_MAX * (SMALL_MAX + 1) * 8);
+  return e;
+}
 
 cudaError_t launch_small_node(const ArenaView& a, const int* items, int count, int mode,
                               int* status, cudaStream_t s) {

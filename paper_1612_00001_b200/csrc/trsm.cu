@@ -243,6 +243,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 int trsm_smem_bytes() { return SMEM_BYTES; }
 
+cudaError_t configure_trsm() {
+  cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  return e;
+}
+
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
                         int blk0, int nblocks, cudaStream_t s) {
   const int nblk = (a.n + T - 1) / T;
@@ -259,14 +266,6 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
                               const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
                               int c_off, int nrhs, bool tri_rhs, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   TrsmArgs p;
   p.base = a.base;
   p.ld = a.ld;
