@@ -299,13 +299,12 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
       if (pub_c || pub_j) {
         fence_proxy_async_smem();   // generic smem writes -> visible to the bulk-copy engine
         __syncwarp();
-        if (lane == 0) {
-          for (int d = 0; d < cs; ++d) {
-            const uint32_t mb = dsmem_addr(&xbar[par], d);
-            if (pub_c) bulk_s2cluster(dsmem_addr(&cmsg[par][rank], d), &cstg[par], sizeof(RowMsg), mb);
-            if (pub_j) bulk_s2cluster(dsmem_addr(&jmsg[par], d), &jstg[par], sizeof(RowMsg), mb);
-          }
-        }
+        // one destination per lane: the bulk copies are issued in parallel
+        if (pub_c && lane < cs)
+          bulk_s2cluster(dsmem_addr(&cmsg[par][rank], lane), &cstg[par], sizeof(RowMsg), dsmem_addr(&xbar[par], lane));
+        if (pub_j && lane >= 16 && lane < 16 + cs)
+          bulk_s2cluster(dsmem_addr(&jmsg[par], lane - 16), &jstg[par], sizeof(RowMsg),
+                         dsmem_addr(&xbar[par], lane - 16));
       }
       PPROF(1);
       mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);

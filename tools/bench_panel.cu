@@ -5,6 +5,7 @@
 #include "../paper_1612_00001_b200/csrc/bri_internal.h"
 using namespace bri;
 int main() {
+  configure_lu();
   const int n = 4096;
   ArenaView a;
   a.n = n; a.ld = n; a.slot_elems = (long long)n * n; a.nslots = 1;

@@ -5,6 +5,7 @@
 namespace bri { void panel_profile_read(unsigned long long* out); void count_launch() {} }
 using namespace bri;
 int main() {
+  configure_lu();
   const int n = 4096;
   ArenaView a; a.n = n; a.ld = n; a.slot_elems = (long long)n * n; a.nslots = 1;
   cudaMalloc(&a.base, sizeof(double) * a.slot_elems);
