@@ -116,6 +116,16 @@ int bri_transpose(bri_arena* arena, void* stream, int count, const int* items);
 int bri_gather_blocks(bri_arena* arena, void* stream, const double* M, long long ldm, int count,
                       const int* items);
 
+/*
+ * Element gather for padded layouts — replaces the shifted-window fetch of
+ * providers.py:203-271,380-402.  Block (i, j) of the view (0-based, order n =
+ * arena order) is [[M, 0], [0, I]] (M: m x m row-major device matrix, leading
+ * dim ldm) at element rows rmap[i*n .. i*n+n) and columns cmap[j*n .. j*n+n)
+ * (device int arrays of length k*n).  items: 3 ints (i, j, destination slot).
+ */
+int bri_gather_elements(bri_arena* arena, void* stream, const double* M, long long ldm, int m,
+                        const int* rmap, const int* cmap, int count, const int* items);
+
 /* FP64 DMMA throughput probe (register-only mma.sync loop on every SM);
  * writes achieved TFLOP/s.  Used by bench.py as the roofline denominator. */
 int bri_fp64_peak(void* stream, int iters, double* tflops);

@@ -35,6 +35,8 @@ SIGNATURES = [
     ("bri_axpby", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_double, _c_double]),
     ("bri_transpose", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT]),
     ("bri_gather_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _P_INT]),
+    ("bri_gather_elements", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _c_void_p, _c_void_p,
+                                     _c_int, _P_INT]),
     ("bri_fp64_peak", _c_int, [_c_void_p, _c_int, ctypes.POINTER(_c_double)]),
 ]
 

@@ -443,6 +443,25 @@ __global__ void gather_kernel(ArenaView a, const double* M, long long ldm, const
   }
 }
 
+// Padded / element-permuted gather: slot (row r, col c) of block (bi, bj) =
+// [[M, 0], [0, I]] at element (rmap[bi*n + r], cmap[bj*n + c]) — the shifted
+// window views of padded layouts (reference providers.py:203-271, 380-402).
+__global__ void gather_elements_kernel(ArenaView a, const double* M, long long ldm, int m, const int* rmap,
+                                       const int* cmap, const int* items) {
+  const int* it = items + 3 * blockIdx.y;
+  const int* rm = rmap + (long long)it[0] * a.n;
+  const int* cm = cmap + (long long)it[1] * a.n;
+  double* dst = a.base + (long long)it[2] * a.slot_elems;
+  for (int r = blockIdx.x; r < a.n; r += gridDim.x) {
+    const int R = rm[r];
+    double* d = dst + (long long)r * a.ld;
+    for (int c = threadIdx.x; c < a.n; c += blockDim.x) {
+      const int C = cm[c];
+      d[c] = (R < m && C < m) ? M[(long long)R * ldm + C] : ((R >= m && R == C) ? 1.0 : 0.0);
+    }
+  }
+}
+
 __global__ void fp64_peak_kernel(double* sink, int iters) {
   double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
   double c[8][2];
@@ -767,6 +786,22 @@ int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ld
   const int gx = ar->v.n < 1024 ? ar->v.n : 1024;
   bri::count_launch();
   gather_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, dev);
+  BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_gather_elements(bri_arena* ar, void* stream, const double* M, long long ldm, int m, const int* rmap,
+                        const int* cmap, int count, const int* items) {
+  if (ar == nullptr || M == nullptr || rmap == nullptr || cmap == nullptr || items == nullptr || count < 0)
+    return fail_msg("bri_gather_elements: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 3 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int gx = ar->v.n < 1024 ? ar->v.n : 1024;
+  bri::count_launch();
+  gather_elements_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, m, rmap, cmap, dev);
   BRI_CHECK(cudaGetLastError());
   return 0;
 }

@@ -156,6 +156,14 @@ class Arena:
                                                  matrix.stride(0), len(items), self._items(flat)),
                       "bri_gather_blocks")
 
+    def gather_elements(self, matrix, m, rmap, cmap, items) -> None:
+        """Padded-view gather: items (block row, block col, slot); rmap/cmap int32 device tensors."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_gather_elements(
+            self.handle, self.stream, ctypes.c_void_p(matrix.data_ptr()), matrix.stride(0), m,
+            ctypes.c_void_p(rmap.data_ptr()), ctypes.c_void_p(cmap.data_ptr()), len(items), self._items(flat)),
+            "bri_gather_elements")
+
     def close(self) -> None:
         if getattr(self, "handle", None) is not None:
             if self.gauge is not None and self._live:

@@ -82,12 +82,28 @@ class _HostSource:
             arena.view(s).copy_(torch.from_numpy(blk), non_blocking=False)
 
 
+class _WindowSource:
+    """Padded layouts: view blocks gathered element-wise from M on the device."""
+
+    def __init__(self, matrix, m: int, b: int, rmap, cmap, device: int):
+        torch = _torch()
+        self.matrix, self.m, self.b = matrix, m, b
+        self.rmap = torch.as_tensor(np.asarray(rmap, dtype=np.int32), device=f"cuda:{device}")
+        self.cmap = torch.as_tensor(np.asarray(cmap, dtype=np.int32), device=f"cuda:{device}")
+
+    def load(self, arena: Arena, items) -> None:
+        arena.gather_elements(self.matrix, self.m, self.rmap, self.cmap, [(i - 1, j - 1, s) for i, j, s in items])
+
+
 def _source_for(provider: BlockProvider, device: int):
     base, mr, mc = provider._base()
     lay = base.layout
-    if lay.l != 0:
-        raise BadPartitionError("padded layouts (l > 0) are not supported on the device path yet")
     dm = base._device_matrix(device)
+    if lay.l != 0:
+        if dm is None:
+            raise BadPartitionError("padded layouts need a memory provider on the device path")
+        ident = np.arange(lay.n)
+        return _WindowSource(dm, lay.m, lay.b, ident, ident, device), base, mr, mc
     src = _DeviceSource(dm, lay.b) if dm is not None else _HostSource(base)
     return src, base, mr, mc
 
@@ -323,9 +339,39 @@ def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots):
     return t0 + t1, i0, s0 + s1
 
 
-def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, invert_roots=True,
-             paths0=None):
+def _execute_padded(provider: BlockProvider, targets, ws: Workspace, trace=None):
+    """Padded layouts (l > 0): each target runs over its own shifted-window view
+    (providers.window_maps, reference providers.py:338-402), then the finisher
+    places the window into the padded output block."""
+    torch = _torch()
     device = ws.device if ws.device is not None else current_device()
+    base, _, _ = provider._base()
+    lay = base.layout
+    dm = base._device_matrix(device)
+    if dm is None:
+        raise BadPartitionError("padded layouts need a memory provider on the device path")
+    out, info = [], None
+    for alpha, beta in targets:
+        view, finish = base.run_view(alpha, beta)
+        src = _WindowSource(dm, lay.m, lay.b, view.rmap, view.cmap, device)
+        sched = build_from_specs(lay.k, [(root_frame(lay.k), None, None)])
+        run = _run_tree if ws.schedule == "tree" else _run_dag
+        tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=True)
+        ws.counters.add_nodes(sched.tree_nodes(0), targets=1)
+        if ws.schedule == "dag":
+            ws.executed.add_nodes(len(sched.nodes), targets=1)
+        else:
+            ws.executed.block_inversions += 1
+        done = finish(tensors[0].cpu().numpy())
+        out.append(torch.from_numpy(done).to(f"cuda:{device}"))
+    return out, info
+
+
+def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, invert_roots=True,
+             paths0=None, targets=None):
+    device = ws.device if ws.device is not None else current_device()
+    if targets is not None and provider._base()[0].layout.l != 0:
+        return _execute_padded(provider, targets, ws, trace)
     src, base, mr, mc = _source_for(provider, device)
     k = base.layout.k
     specs = specs_fn(mr, mc)
@@ -382,7 +428,8 @@ def invert_block(provider: BlockProvider, alpha: int, beta: int, ws: Workspace |
     _check_target(lay, alpha, beta)
     if ws is None:
         ws = Workspace()
-    tensors, _ = _execute(provider, _target_specs(lay.k, [(alpha, beta)]), ws, trace=trace)
+    tensors, _ = _execute(provider, _target_specs(lay.k, [(alpha, beta)]), ws, trace=trace,
+                          targets=[(alpha, beta)])
     return Block(tensors[0], ws)
 
 
@@ -393,7 +440,7 @@ def invert_block_row(provider: BlockProvider, alpha: int, ws: Workspace | None =
     if ws is None:
         ws = Workspace()
     targets = [(alpha, beta) for beta in range(1, lay.k + 1)]
-    tensors, _ = _execute(provider, _target_specs(lay.k, targets), ws)
+    tensors, _ = _execute(provider, _target_specs(lay.k, targets), ws, targets=targets)
     return [Block(t, ws) for t in tensors]
 
 
@@ -404,7 +451,7 @@ def invert_blocks(provider: BlockProvider, targets, ws: Workspace | None = None)
         _check_target(lay, a, b)
     if ws is None:
         ws = Workspace()
-    return _execute(provider, _target_specs(lay.k, list(targets)), ws)
+    return _execute(provider, _target_specs(lay.k, list(targets)), ws, targets=list(targets))
 
 
 @dataclass
@@ -442,7 +489,7 @@ def invert_full(provider: BlockProvider, sink, ws: Workspace | None = None, jobs
     ws.gauge.reset_peak()
     t0 = time.perf_counter()
     targets = [(a, b) for a in range(1, lay.k + 1) for b in range(1, lay.k + 1)]
-    tensors, info = _execute(provider, _target_specs(lay.k, targets), ws)
+    tensors, info = _execute(provider, _target_specs(lay.k, targets), ws, targets=targets)
     for (a, b), t in zip(targets, tensors):
         sink.put(a, b, t)
     wall_ms = (time.perf_counter() - t0) * 1e3

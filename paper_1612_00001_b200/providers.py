@@ -11,8 +11,12 @@ one device kernel (bri_gather_blocks) instead of per-fetch host copies
 (providers.py:318-336 + core.py:92-98).  A CUDA tensor may be passed as the
 matrix to keep M device-resident from the start.
 
-Padded layouts (m not divisible by k, providers.py:203-271) are out of the
-round-1 device scope and rejected with BadPartitionError.
+Padded layouts (m not divisible by k, l > 0): the working matrix is
+[[M, 0], [0, I]] of order m + l.  As in the reference (providers.py:338-402),
+a target's run goes through an element-shifted window view (`window_maps`)
+so that padding rows and columns stay paired in every pivot; the device
+gathers those view blocks straight from M (bri_gather_elements) and a
+finisher places the computed window into the padded output block.
 """
 
 from __future__ import annotations
@@ -25,7 +29,7 @@ from .core import Block, Workspace
 from .errors import BadPartitionError, DimensionMismatchError, IndexOutOfRangeError
 
 __all__ = ["BlockLayout", "BlockPermutation", "BlockProvider", "fetch_block", "make_memory_provider",
-           "permute_provider"]
+           "permute_provider", "window_maps", "window_finisher"]
 
 
 @dataclass(frozen=True)
@@ -92,6 +96,81 @@ class BlockProvider:
         return None
 
 
+def _window_start(lay: BlockLayout, j: int) -> int:
+    """First of b consecutive real indices covering block j's real part."""
+    return min((j - 1) * lay.b, lay.m - lay.b)
+
+
+def window_maps(lay: BlockLayout, alpha: int, beta: int):
+    """Element row / column maps of the shifted-window view for target (alpha, beta).
+
+    The rows lead with beta's b-wide real window, the columns with alpha's;
+    the remaining real indices follow (those outside both windows first, so
+    the two maps agree wherever they can); the l padding indices sit at the
+    same positions in both maps: up to b of them at the very end (last
+    block), any overflow right after the first b - overflow fillers (the
+    anchor block).  Same construction as providers.py:245-271, which keeps
+    every reduction pivot generically nonsingular.
+    """
+    b, m, n, l = lay.b, lay.m, lay.n, lay.l
+    wa, wb = _window_start(lay, alpha), _window_start(lay, beta)
+    idx = np.arange(m)
+    in_a = (idx >= wa) & (idx < wa + b)
+    in_b = (idx >= wb) & (idx < wb + b)
+    shared = idx[~(in_a | in_b)]
+    pad = np.arange(m, n)
+    spill = max(0, l - b)
+
+    def arrange(lead, others):
+        return np.concatenate([lead, others[: b - spill], pad[:spill], others[b - spill:], pad[spill:]])
+
+    rows = arrange(idx[in_b], np.concatenate([shared, idx[in_a & ~in_b]]))
+    cols = arrange(idx[in_a], np.concatenate([shared, idx[in_b & ~in_a]]))
+    return rows, cols
+
+
+def window_finisher(lay: BlockLayout, alpha: int, beta: int):
+    """Map the window result (inverse rows wa.., cols wb..) to the padded block (alpha, beta)."""
+    wa, wb = _window_start(lay, alpha), _window_start(lay, beta)
+
+    def finish(win: np.ndarray) -> np.ndarray:
+        out = np.zeros((lay.b, lay.b))
+        rg = np.arange((alpha - 1) * lay.b, alpha * lay.b)
+        cg = np.arange((beta - 1) * lay.b, beta * lay.b)
+        rr, cc = rg < lay.m, cg < lay.m
+        if rr.any() and cc.any():
+            out[np.ix_(rr, cc)] = win[np.ix_(rg[rr] - wa, cg[cc] - wb)]
+        if alpha == beta:
+            padded = np.flatnonzero(~rr)
+            out[padded, padded] = 1.0
+        return out
+
+    return finish
+
+
+class _WindowView(BlockProvider):
+    """Element-permuted view of [[M, 0], [0, I]] for one padded-target run."""
+
+    def __init__(self, base: "BlockProvider", rmap: np.ndarray, cmap: np.ndarray):
+        self.base = base
+        self.layout = base.layout
+        self.rmap, self.cmap = rmap, cmap
+
+    def _block(self, alpha: int, beta: int) -> np.ndarray:
+        lay = self.layout
+        rows = self.rmap[(alpha - 1) * lay.b: alpha * lay.b]
+        cols = self.cmap[(beta - 1) * lay.b: beta * lay.b]
+        a = self.base.matrix
+        out = np.zeros((rows.size, cols.size))
+        rr, cc = rows < lay.m, cols < lay.m
+        out[np.ix_(rr, cc)] = a[np.ix_(rows[rr], cols[cc])]
+        for i in np.flatnonzero(~rr):
+            hit = np.flatnonzero(cols == rows[i])
+            if hit.size:
+                out[i, hit[0]] = 1.0
+        return out
+
+
 class _MemoryProvider(BlockProvider):
     """Blocks of an in-memory matrix (l = 0); host copy plus a lazily uploaded device copy."""
 
@@ -116,9 +195,6 @@ class _MemoryProvider(BlockProvider):
             m = host.shape[0]
         self._host = host
         self.layout = BlockLayout.for_order(m, k)
-        if self.layout.l != 0:
-            raise BadPartitionError(
-                f"order {m} is not divisible by k={k}: padded layouts are not supported on the device path yet")
 
     @property
     def matrix(self) -> np.ndarray:
@@ -129,8 +205,29 @@ class _MemoryProvider(BlockProvider):
         return self._host
 
     def _block(self, alpha: int, beta: int) -> np.ndarray:
-        b = self.layout.b
-        return self.matrix[(alpha - 1) * b: alpha * b, (beta - 1) * b: beta * b]
+        lay = self.layout
+        b, m = lay.b, lay.m
+        r0, c0 = (alpha - 1) * b, (beta - 1) * b
+        if lay.l == 0 or (r0 + b <= m and c0 + b <= m):
+            return self.matrix[r0:r0 + b, c0:c0 + b]
+        out = np.zeros((b, b))  # block of [[M, 0], [0, I]]
+        nr, nc = max(0, min(b, m - r0)), max(0, min(b, m - c0))
+        if nr and nc:
+            out[:nr, :nc] = self.matrix[r0:r0 + nr, c0:c0 + nc]
+        for g in range(max(r0, c0, m), min(r0 + b, c0 + b)):
+            out[g - r0, g - c0] = 1.0
+        return out
+
+    def run_view(self, alpha: int, beta: int):
+        lay = self.layout
+        if lay.l == 0:
+            return permute_provider(self, alpha, beta), None
+        if lay.k >= 5 and lay.l > 2 * lay.b:
+            raise BadPartitionError(
+                f"order {lay.m} with k={lay.k} needs {lay.l} padding indices, more than two blocks' worth "
+                f"({2 * lay.b}); use a partition with k <= 4 or one that divides the order more evenly")
+        rmap, cmap = window_maps(lay, alpha, beta)
+        return _WindowView(self, rmap, cmap), window_finisher(lay, alpha, beta)
 
     def _device_matrix(self, device: int):
         t = self._dev.get(device)

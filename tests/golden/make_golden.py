@@ -113,7 +113,18 @@ def main():
         arrays[f"inv{n}_matrix"] = x
         arrays[f"inv{n}_out"] = bri.invert_dense(bri.Workspace().from_array(x)).data.copy()
 
-    # 8. exact operation counts k=2..7 (pkg/tests/test_instrumentation.py:42-50)
+    # 8. padded layouts (m % k != 0): shifted-window runs (providers.py:338-402)
+    meta["padded"] = []
+    for m, k, seed in ((10, 4, 88), (13, 4, 13), (30, 8, 30), (50, 6, 51)):
+        a = shifted(m, seed)
+        prov = bri.make_memory_provider(a, k)
+        sink = bri.MemorySink(prov.layout)
+        bri.invert_full(prov, sink)
+        arrays[f"pad_m{m}_k{k}_matrix"] = a
+        arrays[f"pad_m{m}_k{k}_inverse"] = sink.finalize().copy()
+        meta["padded"].append([m, k, seed])
+
+    # 9. exact operation counts k=2..7 (pkg/tests/test_instrumentation.py:42-50)
     meta["counts"] = {str(k): [c.block_inversions, c.block_multiplications, c.block_subtractions,
                                c.schur_nodes] for k in range(2, 8) for c in [bri.predicted_counts(k)]}
 

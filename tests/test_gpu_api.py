@@ -110,8 +110,8 @@ def test_errors_and_edges(bri):
         bri.invert_block(prov, 0, 1)
     with pytest.raises(bri.IndexOutOfRangeError):
         bri.invert_block(prov, 1, 3)
-    with pytest.raises(bri.BadPartitionError):
-        bri.make_memory_provider(shifted(10, 1), 4)  # padded layouts: not on the device path yet
+    with pytest.raises(bri.BadPartitionError):  # k >= 5 with more than 2b padding (providers.py:342-351)
+        bri.invert_block(bri.make_memory_provider(shifted(9, 1), 8), 1, 1)
     with pytest.raises(bri.SingularPivotError):  # exact I: off-diagonal pivots are singular
         bri.invert_block(bri.make_memory_provider(np.eye(6), 3), 1, 2)
     ws = bri.Workspace()
@@ -135,3 +135,24 @@ def test_device_and_host_inputs_agree(bri):
     pin = bri.invert_block(bri.make_memory_provider(torch.from_numpy(a).pin_memory(), 2), 2, 1).data
     np.testing.assert_array_equal(host, dev)
     np.testing.assert_array_equal(host, pin)
+
+
+def test_padded_layouts_match_reference(bri, golden):
+    """m % k != 0: shifted-window views (providers.py:338-402) vs the reference's own full inverse."""
+    data, meta = golden
+    for m, k, seed in meta["padded"]:
+        a = data[f"pad_m{m}_k{k}_matrix"]
+        prov = bri.make_memory_provider(a, k)
+        sink = bri.MemorySink(prov.layout)
+        s = bri.invert_full(prov, sink)
+        got = sink.finalize()
+        ref = data[f"pad_m{m}_k{k}_inverse"]
+        assert got.shape == (m, m) and s.l == (-m) % k
+        assert np.abs(got - ref).max() <= 1e-9 * np.abs(ref).max(), (m, k)
+        assert np.abs(a @ got - np.eye(m)).max() <= 1e-9
+    # single block + tree schedule agree with the DAG schedule
+    a = data["pad_m13_k4_matrix"]
+    prov = bri.make_memory_provider(a, 4)
+    x = bri.invert_block(prov, 4, 2).data
+    y = bri.invert_block(prov, 4, 2, bri.Workspace(schedule="tree")).data
+    np.testing.assert_allclose(x, y, rtol=0, atol=1e-12)
