@@ -1,20 +1,93 @@
-"""Output sinks (reference formats.py:249-282).
+"""Sinks and the BRIM matrix file (reference formats.py:49-282).
 
 `sink.put(alpha, beta, block)` accepts an ndarray, a torch tensor or an object
-with `.data`, in any order and from any thread; `finalize()` returns the
-assembled inverse or raises MissingBlocksError.  BRIM files are out of the
-round-1 scope.
+with `.data`, in any order and from any thread; `finalize()` completes the
+output or raises MissingBlocksError.
+
+BRIM (the reference's on-disk format, formats.py:1-14): a 24-byte
+little-endian header — magic b"BRIM", u32 version, u64 order m, u8 dtype tag
+(1 = float64), 7 reserved bytes — followed by m*m row-major float64.  A sink
+writes version 0 first and stamps version 1 only in `finalize()`, so a
+partial file is detectable; readers reject version 0.  `make_file_provider`
+(providers.py) reads BRIM inputs through a memory map.
 """
 
 from __future__ import annotations
 
+import os
+import struct
 import threading
+from dataclasses import dataclass
 
 import numpy as np
 
-from .errors import IndexOutOfRangeError, MissingBlocksError
+from .errors import DimensionMismatchError, FormatError, IndexOutOfRangeError, MissingBlocksError
 
-__all__ = ["MemorySink"]
+__all__ = ["MemorySink", "BrimSink", "BrimHeader", "write_matrix", "read_header", "read_matrix",
+           "open_matrix", "MAGIC", "VERSION", "HEADER_BYTES"]
+
+MAGIC = b"BRIM"
+VERSION = 1
+DTYPE_F64 = 1
+HEADER_BYTES = 24
+_LAYOUT = struct.Struct("<4sIQB7x")
+
+
+@dataclass(frozen=True)
+class BrimHeader:
+    m: int
+    version: int = VERSION
+    dtype_tag: int = DTYPE_F64
+
+    def pack(self) -> bytes:
+        return _LAYOUT.pack(MAGIC, self.version, self.m, self.dtype_tag)
+
+    @property
+    def total_bytes(self) -> int:
+        return HEADER_BYTES + 8 * self.m * self.m
+
+
+def _parse(raw: bytes, where: str) -> BrimHeader:
+    if len(raw) < HEADER_BYTES:
+        raise FormatError(f"{where}: truncated header ({len(raw)} of {HEADER_BYTES} bytes)")
+    magic, version, m, tag = _LAYOUT.unpack(raw[:HEADER_BYTES])
+    if magic != MAGIC:
+        raise FormatError(f"{where}: bad magic {magic!r}, expected {MAGIC!r}")
+    if version != VERSION:
+        hint = " (version 0 marks a partial or aborted write)" if version == 0 else ""
+        raise FormatError(f"{where}: unsupported version {version}{hint}")
+    if tag != DTYPE_F64:
+        raise FormatError(f"{where}: unsupported dtype tag {tag}, expected {DTYPE_F64}")
+    return BrimHeader(m=int(m))
+
+
+def read_header(path) -> BrimHeader:
+    path = os.fspath(path)
+    with open(path, "rb") as fh:
+        head = _parse(fh.read(HEADER_BYTES), path)
+        size = fh.seek(0, os.SEEK_END)
+    if size != head.total_bytes:
+        raise FormatError(f"{path}: expected {head.total_bytes} bytes for order {head.m}, found {size}")
+    return head
+
+
+def write_matrix(path, matrix) -> None:
+    a = np.ascontiguousarray(matrix, dtype="<f8")
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise DimensionMismatchError(f"matrix must be square, got shape {a.shape}")
+    with open(os.fspath(path), "wb") as fh:
+        fh.write(BrimHeader(m=a.shape[0]).pack())
+        a.tofile(fh)
+
+
+def open_matrix(path) -> np.ndarray:
+    """Read-only memory map of a BRIM payload as an (m, m) float64 array."""
+    head = read_header(path)
+    return np.memmap(os.fspath(path), dtype="<f8", mode="r", offset=HEADER_BYTES, shape=(head.m, head.m))
+
+
+def read_matrix(path) -> np.ndarray:
+    return np.array(open_matrix(path), dtype=np.float64)
 
 
 def _as_host(block) -> np.ndarray:
@@ -28,12 +101,13 @@ def _as_host(block) -> np.ndarray:
     return np.asarray(getattr(block, "data", block))
 
 
-class MemorySink:
-    """Collect inverse blocks into a host (m, m) array."""
+class _BlockSink:
+    """Shared put/finalize bookkeeping: validates (alpha, beta) and the block
+    shape, trims the augmentation padding, and records arrivals; subclasses
+    provide the (m, m) row-major `self._canvas` the trimmed block lands in."""
 
     def __init__(self, layout):
         self.layout = layout
-        self.canvas = np.zeros((layout.m, layout.m))
         self._received: set = set()
         self._lock = threading.Lock()
 
@@ -42,17 +116,80 @@ class MemorySink:
         if not (1 <= alpha <= lay.k and 1 <= beta <= lay.k):
             raise IndexOutOfRangeError(f"block ({alpha}, {beta}) outside 1..{lay.k}")
         data = _as_host(block)
+        if data.shape != (lay.b, lay.b):
+            raise DimensionMismatchError(f"block ({alpha}, {beta}) has shape {data.shape}, "
+                                         f"expected ({lay.b}, {lay.b})")
         r0, c0 = (alpha - 1) * lay.b, (beta - 1) * lay.b
-        nr, nc = min(lay.b, lay.m - r0), min(lay.b, lay.m - c0)
+        r1, c1 = min(r0 + lay.b, lay.m), min(c0 + lay.b, lay.m)
         with self._lock:
-            if nr > 0 and nc > 0:
-                self.canvas[r0:r0 + nr, c0:c0 + nc] = data[:nr, :nc]
+            if r1 > r0 and c1 > c0:
+                self._canvas[r0:r1, c0:c1] = data[: r1 - r0, : c1 - c0]
             self._received.add((alpha, beta))
 
-    def finalize(self) -> np.ndarray:
-        lay = self.layout
-        missing = [(a, b) for a in range(1, lay.k + 1) for b in range(1, lay.k + 1)
-                   if (a, b) not in self._received]
+    def _check_complete(self) -> None:
+        k = self.layout.k
+        missing = [(a, b) for a in range(1, k + 1) for b in range(1, k + 1) if (a, b) not in self._received]
         if missing:
             raise MissingBlocksError(missing)
-        return self.canvas
+
+
+class BrimSink(_BlockSink):
+    """Stream inverse blocks into a BRIM file (padding trimmed).
+
+    The payload is a writable memory map over the file, so a put is one
+    strided copy; the header carries version 0 until `finalize()` has seen
+    all k*k blocks, then version 1 is written in place.  Closing without
+    finalizing (or leaving the context on an exception) keeps the marker.
+    """
+
+    def __init__(self, path, layout):
+        super().__init__(layout)
+        self.path = os.fspath(path)
+        m = layout.m
+        with open(self.path, "wb") as fh:
+            fh.write(BrimHeader(m=m, version=0).pack())
+            fh.truncate(HEADER_BYTES + 8 * m * m)
+        self._canvas = np.memmap(self.path, dtype="<f8", mode="r+", offset=HEADER_BYTES, shape=(m, m))
+        self._finalized = False
+
+    def finalize(self) -> None:
+        self._check_complete()
+        with self._lock:
+            self._canvas.flush()
+            fd = os.open(self.path, os.O_WRONLY)
+            try:
+                os.pwrite(fd, BrimHeader(m=self.layout.m).pack(), 0)
+            finally:
+                os.close(fd)
+            self._finalized = True
+
+    def close(self) -> None:
+        if self._canvas is not None:
+            self._canvas.flush()
+            self._canvas = None
+
+    def __enter__(self) -> "BrimSink":
+        return self
+
+    def __exit__(self, exc_type, exc, tb) -> None:
+        try:
+            if exc_type is None and not self._finalized:
+                self.finalize()
+        finally:
+            self.close()
+
+
+class MemorySink(_BlockSink):
+    """Collect inverse blocks into a host (m, m) array."""
+
+    def __init__(self, layout):
+        super().__init__(layout)
+        self._canvas = np.zeros((layout.m, layout.m))
+
+    @property
+    def canvas(self) -> np.ndarray:
+        return self._canvas
+
+    def finalize(self) -> np.ndarray:
+        self._check_complete()
+        return self._canvas

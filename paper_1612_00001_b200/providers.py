@@ -29,7 +29,7 @@ from .core import Block, Workspace
 from .errors import BadPartitionError, DimensionMismatchError, IndexOutOfRangeError
 
 __all__ = ["BlockLayout", "BlockPermutation", "BlockProvider", "fetch_block", "make_memory_provider",
-           "permute_provider", "window_maps", "window_finisher"]
+           "permute_provider", "window_maps", "window_finisher", "make_file_provider"]
 
 
 @dataclass(frozen=True)
@@ -237,7 +237,7 @@ class _MemoryProvider(BlockProvider):
             if self._pinned is not None:  # pinned host tensor: one async H2D copy
                 t = self._pinned.to(f"cuda:{device}", non_blocking=True)
             else:
-                src = torch.from_numpy(np.array(self.matrix, copy=True))
+                src = torch.from_numpy(np.array(self.matrix, dtype=np.float64, copy=True))
                 t = src.pin_memory().to(f"cuda:{device}", non_blocking=True)
             self._dev[device] = t
         return t
@@ -269,6 +269,27 @@ def fetch_block(provider: BlockProvider, alpha: int, beta: int, ws: Workspace | 
 def make_memory_provider(matrix, k: int) -> BlockProvider:
     """Provider over an in-memory square matrix (numpy array or torch tensor)."""
     return _MemoryProvider(matrix, k)
+
+
+class _FileProvider(_MemoryProvider):
+    """BRIM file input (providers.py:166-172, 473-476): a read-only memory map;
+    the device path uploads it once (the OS pages it in), host fetches read
+    only the requested rows."""
+
+    def __init__(self, path, k: int):
+        from .formats import open_matrix
+
+        mm = open_matrix(path)
+        self._host = mm
+        self._dev = {}
+        self._pinned = None
+        self.path = path
+        self.layout = BlockLayout.for_order(mm.shape[0], k)
+
+
+def make_file_provider(path, k: int) -> BlockProvider:
+    """Provider over a BRIM file."""
+    return _FileProvider(path, k)
 
 
 def permute_provider(provider: BlockProvider, alpha: int, beta: int) -> BlockProvider:

@@ -156,3 +156,31 @@ def test_padded_layouts_match_reference(bri, golden):
     x = bri.invert_block(prov, 4, 2).data
     y = bri.invert_block(prov, 4, 2, bri.Workspace(schedule="tree")).data
     np.testing.assert_allclose(x, y, rtol=0, atol=1e-12)
+
+
+def test_file_round_trip_criterion_10(bri, tmp_path):
+    """BRIM in, BRIM out (pkg/tests/test_acceptance.py:222-243): the file and memory
+    providers give byte-identical inverse files, and the result matches the oracle."""
+    from conftest import oracle_with_floor, rel_err
+
+    for m, k, seed in ((12, 3, 91), (256, 4, 3), (130, 4, 7)):
+        a = shifted(m, seed)
+        src = tmp_path / f"m{m}.brim"
+        bri.write_matrix(src, a)
+        prov_f = bri.make_file_provider(src, k)
+        out_f, out_m = tmp_path / f"f{m}.brim", tmp_path / f"mem{m}.brim"
+        with bri.BrimSink(out_f, prov_f.layout) as sink:
+            bri.invert_full(prov_f, sink)
+        prov_m = bri.make_memory_provider(a, k)
+        with bri.BrimSink(out_m, prov_m.layout) as sink:
+            bri.invert_full(prov_m, sink)
+        assert out_f.read_bytes() == out_m.read_bytes(), m
+        got = bri.read_matrix(out_f)
+        assert got.shape == (m, m)
+        assert np.abs(a @ got - np.eye(m)).max() <= 1e-9
+        if m % k == 0:
+            refs, floor = oracle_with_floor(a, k, [(1, 1), (k, 2)])
+            b = m // k
+            for (al, be), ref in refs.items():
+                blk = got[(al - 1) * b:al * b, (be - 1) * b:be * b]
+                assert rel_err(blk, ref) <= max(1e-9, 8 * floor[(al, be)]), (m, al, be)

@@ -145,3 +145,94 @@ def test_no_cpu_fallback_without_device():
 
     with pytest.raises(p.DeviceError):
         p.invert_block(p.make_memory_provider(shifted(8, 1), 2), 1, 1)
+
+
+def test_brim_format_round_trip(tmp_path):
+    """BRIM bytes (pkg/tests/test_formats.py, test_acceptance.py:222-243 first half)."""
+    import struct
+
+    from paper_1612_00001_b200 import formats
+    from paper_1612_00001_b200.errors import FormatError
+
+    a = shifted(12, 91)
+    src = tmp_path / "m.brim"
+    formats.write_matrix(src, a)
+    raw = src.read_bytes()
+    assert len(raw) == 24 + 8 * 144
+    assert struct.unpack("<4sIQB", raw[:17]) == (b"BRIM", 1, 12, 1) and raw[17:24] == bytes(7)
+    assert formats.read_header(src).m == 12
+    np.testing.assert_array_equal(formats.read_matrix(src), a)
+    copy = tmp_path / "c.brim"
+    formats.write_matrix(copy, formats.read_matrix(src))
+    assert raw == copy.read_bytes()
+    for name, blob in (("magic", b"XXXX" + raw[4:]), ("short", raw[:-8]), ("tag", raw[:16] + b"\x02" + raw[17:]),
+                       ("version", raw[:4] + struct.pack("<I", 7) + raw[8:]), ("header", raw[:10])):
+        bad = tmp_path / f"{name}.brim"
+        bad.write_bytes(blob)
+        with pytest.raises(FormatError):
+            formats.read_matrix(bad)
+    with pytest.raises(Exception):
+        formats.write_matrix(tmp_path / "rect.brim", np.zeros((2, 3)))
+
+
+def test_brim_sink(tmp_path):
+    """BrimSink contract (pkg/tests/test_formats.py:111-180): trimming, any order,
+    partial marker, completeness and shape/index checks."""
+    from paper_1612_00001_b200 import formats
+    from paper_1612_00001_b200.errors import (DimensionMismatchError, FormatError, IndexOutOfRangeError,
+                                              MissingBlocksError)
+    from paper_1612_00001_b200.providers import BlockLayout
+
+    lay = BlockLayout.for_order(10, 4)
+    full = np.random.default_rng(5).standard_normal((12, 12))
+    out = tmp_path / "inv.brim"
+    with formats.BrimSink(out, lay) as sink:
+        for al in (4, 2, 3, 1):
+            for be in (1, 3, 2, 4):
+                sink.put(al, be, full[(al - 1) * 3:al * 3, (be - 1) * 3:be * 3])
+        sink.put(1, 1, full[:3, :3])  # repeated put
+    got = formats.read_matrix(out)
+    assert got.shape == (10, 10)
+    np.testing.assert_array_equal(got, full[:10, :10])
+
+    lay2 = BlockLayout.for_order(4, 2)
+    part = tmp_path / "part.brim"
+    sink = formats.BrimSink(part, lay2)
+    sink.put(1, 1, np.eye(2))
+    for al, be in ((1, 2), (2, 1)):
+        sink.put(al, be, np.zeros((2, 2)))
+    with pytest.raises(MissingBlocksError) as exc:
+        sink.finalize()
+    assert exc.value.missing == [(2, 2)]
+    with pytest.raises(DimensionMismatchError):
+        sink.put(1, 1, np.zeros((3, 3)))
+    with pytest.raises(IndexOutOfRangeError):
+        sink.put(0, 1, np.zeros((2, 2)))
+    sink.close()
+    assert part.read_bytes()[4:8] == bytes(4)
+    with pytest.raises(FormatError, match="partial"):
+        formats.read_matrix(part)
+
+    with pytest.raises(RuntimeError):  # an exception inside the context keeps the marker
+        with formats.BrimSink(part, lay2) as sink:
+            for al in (1, 2):
+                for be in (1, 2):
+                    sink.put(al, be, np.ones((2, 2)))
+            raise RuntimeError("abort")
+    with pytest.raises(FormatError):
+        formats.read_header(part)
+
+
+def test_file_provider_blocks_match_memory(tmp_path):
+    """make_file_provider == make_memory_provider block for block (pkg/tests/test_providers.py:70-97)."""
+    from paper_1612_00001_b200 import formats, make_file_provider, make_memory_provider
+
+    for m, k in ((6, 3), (64, 4), (10, 4)):
+        a = np.random.default_rng(22 + m).standard_normal((m, m))
+        path = tmp_path / f"a{m}.brim"
+        formats.write_matrix(path, a)
+        mem, fil = make_memory_provider(a, k), make_file_provider(path, k)
+        assert fil.layout == mem.layout
+        for al in range(1, k + 1):
+            for be in range(1, k + 1):
+                np.testing.assert_array_equal(np.asarray(fil._block(al, be)), mem._block(al, be))
