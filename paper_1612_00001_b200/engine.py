@@ -69,17 +69,48 @@ class _DeviceSource:
 
 
 class _HostSource:
-    """Generic provider: blocks read through `_block` and copied host -> device."""
+    """Generic and out-of-core providers: blocks read through `_block` into a
+    ring of pinned staging buffers by reader threads, then copied host -> device
+    asynchronously on the run's stream, so the read (page cache, disk or a
+    Python provider) of the next blocks overlaps the H2D copy of this one.
+    A buffer is reused only after the copy that drained it has completed."""
+
+    RING = 4
 
     def __init__(self, provider: BlockProvider):
         self.provider = provider
         self.b = provider.layout.b
+        self._bufs = None
+        self._events = [None] * self.RING
+
+    def _read(self, idx: int, ij) -> None:
+        ev = self._events[idx]
+        if ev is not None:
+            ev.synchronize()
+        np.copyto(self._bufs[idx].numpy(), self.provider._block(*ij), casting="unsafe")
 
     def load(self, arena: Arena, items) -> None:
+        from concurrent.futures import ThreadPoolExecutor
+
         torch = _torch()
-        for i, j, s in items:
-            blk = np.ascontiguousarray(self.provider._block(i, j), dtype=np.float64)
-            arena.view(s).copy_(torch.from_numpy(blk), non_blocking=False)
+        items = list(items)
+        if not items:
+            return
+        R = self.RING
+        if self._bufs is None:
+            self._bufs = [torch.empty((self.b, self.b), dtype=torch.float64).pin_memory() for _ in range(R)]
+        stream = torch.cuda.current_stream(arena.device)
+        with ThreadPoolExecutor(max_workers=R) as pool:
+            pending = {n: pool.submit(self._read, n % R, items[n][:2]) for n in range(min(R, len(items)))}
+            for n, (_, _, s) in enumerate(items):
+                pending.pop(n).result()
+                idx = n % R
+                arena.view(s).copy_(self._bufs[idx], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self._events[idx] = ev
+                if n + R < len(items):
+                    pending[n + R] = pool.submit(self._read, idx, items[n + R][:2])
 
 
 class _WindowSource:
@@ -101,7 +132,7 @@ def _source_for(provider: BlockProvider, device: int):
     dm = base._device_matrix(device)
     if lay.l != 0:
         if dm is None:
-            raise BadPartitionError("padded layouts need a memory provider on the device path")
+            return _HostSource(base), base, mr, mc
         ident = np.arange(lay.n)
         return _WindowSource(dm, lay.m, lay.b, ident, ident, device), base, mr, mc
     src = _DeviceSource(dm, lay.b) if dm is not None else _HostSource(base)
@@ -348,12 +379,13 @@ def _execute_padded(provider: BlockProvider, targets, ws: Workspace, trace=None)
     base, _, _ = provider._base()
     lay = base.layout
     dm = base._device_matrix(device)
-    if dm is None:
-        raise BadPartitionError("padded layouts need a memory provider on the device path")
     out, info = [], None
     for alpha, beta in targets:
         view, finish = base.run_view(alpha, beta)
-        src = _WindowSource(dm, lay.m, lay.b, view.rmap, view.cmap, device)
+        if dm is not None:
+            src = _WindowSource(dm, lay.m, lay.b, view.rmap, view.cmap, device)
+        else:  # M does not fit in HBM: stream the view's blocks from the host
+            src = _HostSource(view)
         sched = build_from_specs(lay.k, [(root_frame(lay.k), None, None)])
         run = _run_tree if ws.schedule == "tree" else _run_dag
         tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=True)

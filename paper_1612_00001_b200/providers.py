@@ -171,6 +171,32 @@ class _WindowView(BlockProvider):
         return out
 
 
+RESIDENT_FRACTION = 0.5
+
+
+def upload_rows(host: np.ndarray, device: int, chunk_bytes: int = 64 << 20):
+    """Host (m, n) array -> CUDA float64 tensor through two pinned staging
+    chunks: the host-side copy of chunk c+1 (a memory map reads the file here)
+    overlaps the H2D copy of chunk c, and nothing the size of M is pinned."""
+    import torch
+
+    m, n = host.shape
+    dst = torch.empty((m, n), dtype=torch.float64, device=f"cuda:{device}")
+    rows = max(1, min(m, chunk_bytes // (8 * max(n, 1))))
+    bufs = [torch.empty((rows, n), dtype=torch.float64).pin_memory() for _ in range(2)]
+    done = [None, None]
+    stream = torch.cuda.current_stream(device)
+    for c, r0 in enumerate(range(0, m, rows)):
+        idx, r1 = c % 2, min(m, r0 + rows)
+        if done[idx] is not None:
+            done[idx].synchronize()
+        np.copyto(bufs[idx][: r1 - r0].numpy(), host[r0:r1], casting="unsafe")
+        dst[r0:r1].copy_(bufs[idx][: r1 - r0], non_blocking=True)
+        done[idx] = torch.cuda.Event()
+        done[idx].record(stream)
+    return dst
+
+
 class _MemoryProvider(BlockProvider):
     """Blocks of an in-memory matrix (l = 0); host copy plus a lazily uploaded device copy."""
 
@@ -230,15 +256,22 @@ class _MemoryProvider(BlockProvider):
         return _WindowView(self, rmap, cmap), window_finisher(lay, alpha, beta)
 
     def _device_matrix(self, device: int):
+        """M resident in HBM (uploaded once), or None when it would take more
+        than RESIDENT_FRACTION of the free device memory: the engine then
+        streams blocks from the host instead (out-of-core)."""
         t = self._dev.get(device)
         if t is None:
             import torch
 
+            m = self.layout.m
+            free, _ = torch.cuda.mem_get_info(device)
+            spare = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+            if 8 * m * m > RESIDENT_FRACTION * (free + spare):
+                return None
             if self._pinned is not None:  # pinned host tensor: one async H2D copy
                 t = self._pinned.to(f"cuda:{device}", non_blocking=True)
             else:
-                src = torch.from_numpy(np.array(self.matrix, dtype=np.float64, copy=True))
-                t = src.pin_memory().to(f"cuda:{device}", non_blocking=True)
+                t = upload_rows(self.matrix, device)
             self._dev[device] = t
         return t
 
@@ -272,9 +305,11 @@ def make_memory_provider(matrix, k: int) -> BlockProvider:
 
 
 class _FileProvider(_MemoryProvider):
-    """BRIM file input (providers.py:166-172, 473-476): a read-only memory map;
-    the device path uploads it once (the OS pages it in), host fetches read
-    only the requested rows."""
+    """BRIM file input (providers.py:166-172, 473-476) over a read-only memory map.
+
+    When M fits the device it is streamed once into HBM through pinned staging
+    chunks (`upload_rows`); otherwise the engine's host source reads only the
+    blocks a run needs, through its pinned ring, straight from the map."""
 
     def __init__(self, path, k: int):
         from .formats import open_matrix
