@@ -126,6 +126,27 @@ int bri_gather_blocks(bri_arena* arena, void* stream, const double* M, long long
 int bri_gather_elements(bri_arena* arena, void* stream, const double* M, long long ldm, int m,
                         const int* rmap, const int* cmap, int count, const int* items);
 
+/*
+ * LS-SVM kernel system matrix generated on the device — replaces the
+ * per-fetch element evaluation of providers.py:175-200 (_KernelSource.rect,
+ * KernelSpec providers.py:93-120).  x: n x d row-major device inputs; the
+ * matrix has order m = n + 1: (0,0) = 0, the rest of row/column 0 = 1,
+ * interior (i, j) = exp(sq_ij / denom) + (i == j ? ridge : 0) with sq_ij the
+ * squared distance of inputs i-1 and j-1 summed in numpy's pairwise order,
+ * denom = -2 sigma^2 and ridge = 1 / gamma as the caller computes them.
+ * Indices >= m are the identity padding of [[M, 0], [0, I]].
+ *
+ * bri_rbf_blocks writes view blocks (i, j) of order n_arena into slots —
+ * items: 3 ints (block row, block col, slot), 0-based — with element rows
+ * rmap[i*n_arena + r] and columns cmap[j*n_arena + c] (device int arrays, or
+ * both NULL for the identity view).  bri_rbf_dense writes the whole m x m
+ * matrix row-major into out (leading dim ldo >= m).
+ */
+int bri_rbf_blocks(bri_arena* arena, void* stream, const double* x, int n, int d, double denom, double ridge,
+                   const int* rmap, const int* cmap, int count, const int* items);
+int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, double ridge, double* out,
+                  long long ldo);
+
 /* FP64 DMMA throughput probe (register-only mma.sync loop on every SM);
  * writes achieved TFLOP/s.  Used by bench.py as the roofline denominator. */
 int bri_fp64_peak(void* stream, int iters, double* tflops);

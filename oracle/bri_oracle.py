@@ -281,6 +281,23 @@ def lu_invert_full(a: np.ndarray) -> np.ndarray:
     return invert_dense(a)
 
 
+def kernel_matrix(inputs: np.ndarray, gamma: float = 1.0, sigma: float = 1.0) -> np.ndarray:
+    """LS-SVM system matrix of order n + 1 (providers.py:93-120 element rule,
+    evaluated like _KernelSource.rect providers.py:182-200): 0 at (1,1), ones on
+    the rest of the first row/column, Gaussian Gram + ridge 1/gamma inside."""
+    x = np.ascontiguousarray(inputs, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+    m = x.shape[0] + 1
+    out = np.ones((m, m))
+    out[0, 0] = 0.0
+    sq = ((x[:, None, :] - x[None, :, :]) ** 2).sum(axis=2)
+    gram = np.exp(sq / (-2.0 * sigma ** 2))
+    gram[np.diag_indices(m - 1)] += 1.0 / gamma
+    out[1:, 1:] = gram
+    return out
+
+
 def predicted_nodes(k: int) -> int:
     """(4^(k-1) - 1) / 3 Schur nodes per target (instrumentation.py:124-139)."""
     return (4 ** (k - 1) - 1) // 3

@@ -37,6 +37,9 @@ SIGNATURES = [
     ("bri_gather_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _P_INT]),
     ("bri_gather_elements", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _c_void_p, _c_void_p,
                                      _c_int, _P_INT]),
+    ("bri_rbf_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_double, _c_double,
+                                _c_void_p, _c_void_p, _c_int, _P_INT]),
+    ("bri_rbf_dense", _c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_void_p, _c_ll]),
     ("bri_fp64_peak", _c_int, [_c_void_p, _c_int, ctypes.POINTER(_c_double)]),
 ]
 

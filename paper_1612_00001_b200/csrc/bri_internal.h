@@ -94,4 +94,17 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
 cudaError_t launch_small_node(const ArenaView& a, const int* items, int count, int mode,
                               int* status, cudaStream_t s);
 
+// LS-SVM kernel system matrix generated on the device (generate.cu).
+struct RbfArgs {
+  const double* x;  // n x d row-major training inputs (device)
+  int n, d;
+  double denom;     // -2 sigma^2
+  double ridge;     // 1 / gamma
+  const int* rmap;  // device view->global maps of length k*bn, or nullptr (identity)
+  const int* cmap;
+};
+// items: (block row, block col, slot) device triples; nullptr = one dense output at base.
+cudaError_t launch_rbf(const RbfArgs& g, double* base, long long slot_elems, int ld, int bn, const int* items,
+                       int count, cudaStream_t s);
+
 }  // namespace bri

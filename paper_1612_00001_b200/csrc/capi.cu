@@ -806,6 +806,30 @@ int bri_gather_elements(bri_arena* ar, void* stream, const double* M, long long 
   return 0;
 }
 
+int bri_rbf_blocks(bri_arena* ar, void* stream, const double* x, int n, int d, double denom, double ridge,
+                   const int* rmap, const int* cmap, int count, const int* items) {
+  if (ar == nullptr || x == nullptr || items == nullptr || n < 1 || d < 1 || count < 0 ||
+      (rmap == nullptr) != (cmap == nullptr))
+    return fail_msg("bri_rbf_blocks: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 3 * count);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const RbfArgs g{x, n, d, denom, ridge, rmap, cmap};
+  BRI_CHECK(launch_rbf(g, ar->v.base, ar->v.slot_elems, ar->v.ld, ar->v.n, dev, count, s));
+  return 0;
+}
+
+int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, double ridge, double* out,
+                  long long ldo) {
+  if (x == nullptr || out == nullptr || n < 1 || d < 1 || ldo < (long long)n + 1 || ldo > 0x7fffffffLL)
+    return fail_msg("bri_rbf_dense: bad arguments");
+  const RbfArgs g{x, n, d, denom, ridge, nullptr, nullptr};
+  BRI_CHECK(launch_rbf(g, out, 0, (int)ldo, n + 1, nullptr, 1, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 int bri_fp64_peak(void* stream, int iters, double* tflops) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0, sms = 0;

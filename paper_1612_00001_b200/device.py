@@ -164,6 +164,17 @@ class Arena:
             ctypes.c_void_p(rmap.data_ptr()), ctypes.c_void_p(cmap.data_ptr()), len(items), self._items(flat)),
             "bri_gather_elements")
 
+    def rbf(self, gen, items, rmap=None, cmap=None) -> None:
+        """Generate kernel-matrix view blocks into slots (gen: providers.KernelGenerator);
+        items (block row, block col, slot), 0-based; rmap/cmap int32 device tensors or None."""
+        flat = [s for it in items for s in it]
+        x = gen.inputs_on(self.device)
+        _native.check(self.lib.bri_rbf_blocks(
+            self.handle, self.stream, ctypes.c_void_p(x.data_ptr()), gen.n, gen.d, gen.denom, gen.ridge,
+            ctypes.c_void_p(rmap.data_ptr()) if rmap is not None else None,
+            ctypes.c_void_p(cmap.data_ptr()) if cmap is not None else None, len(items), self._items(flat)),
+            "bri_rbf_blocks")
+
     def close(self) -> None:
         if getattr(self, "handle", None) is not None:
             if self.gauge is not None and self._live:

@@ -126,9 +126,27 @@ class _WindowSource:
         arena.gather_elements(self.matrix, self.m, self.rmap, self.cmap, [(i - 1, j - 1, s) for i, j, s in items])
 
 
+class _GenSource:
+    """Generated providers (LS-SVM kernel matrix): blocks computed straight
+    into their slots on the device; maps select a padded window view."""
+
+    def __init__(self, gen, b: int, rmap, cmap, device: int):
+        torch = _torch()
+        self.gen, self.b = gen, b
+        self.rmap = self.cmap = None
+        if rmap is not None:
+            self.rmap = torch.as_tensor(np.asarray(rmap, dtype=np.int32), device=f"cuda:{device}")
+            self.cmap = torch.as_tensor(np.asarray(cmap, dtype=np.int32), device=f"cuda:{device}")
+
+    def load(self, arena: Arena, items) -> None:
+        arena.rbf(self.gen, [(i - 1, j - 1, s) for i, j, s in items], self.rmap, self.cmap)
+
+
 def _source_for(provider: BlockProvider, device: int):
     base, mr, mc = provider._base()
     lay = base.layout
+    if hasattr(base, "_generator"):
+        return _GenSource(base._generator(), lay.b, None, None, device), base, mr, mc
     dm = base._device_matrix(device)
     if lay.l != 0:
         if dm is None:
@@ -378,11 +396,14 @@ def _execute_padded(provider: BlockProvider, targets, ws: Workspace, trace=None)
     device = ws.device if ws.device is not None else current_device()
     base, _, _ = provider._base()
     lay = base.layout
-    dm = base._device_matrix(device)
+    gen = base._generator() if hasattr(base, "_generator") else None
+    dm = None if gen is not None else base._device_matrix(device)
     out, info = [], None
     for alpha, beta in targets:
         view, finish = base.run_view(alpha, beta)
-        if dm is not None:
+        if gen is not None:
+            src = _GenSource(gen, lay.b, view.rmap, view.cmap, device)
+        elif dm is not None:
             src = _WindowSource(dm, lay.m, lay.b, view.rmap, view.cmap, device)
         else:  # M does not fit in HBM: stream the view's blocks from the host
             src = _HostSource(view)

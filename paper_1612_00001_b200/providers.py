@@ -29,7 +29,8 @@ from .core import Block, Workspace
 from .errors import BadPartitionError, DimensionMismatchError, IndexOutOfRangeError
 
 __all__ = ["BlockLayout", "BlockPermutation", "BlockProvider", "fetch_block", "make_memory_provider",
-           "permute_provider", "window_maps", "window_finisher", "make_file_provider"]
+           "permute_provider", "window_maps", "window_finisher", "make_file_provider", "KernelSpec",
+           "make_kernel_provider", "kernel_matrix"]
 
 
 @dataclass(frozen=True)
@@ -160,7 +161,15 @@ class _WindowView(BlockProvider):
         lay = self.layout
         rows = self.rmap[(alpha - 1) * lay.b: alpha * lay.b]
         cols = self.cmap[(beta - 1) * lay.b: beta * lay.b]
-        a = self.base.matrix
+        return self.base._elements(rows, cols)
+
+
+class _MatrixElements:
+    """Element access to [[M, 0], [0, I]] for window views of a stored M."""
+
+    def _elements(self, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+        lay = self.layout
+        a = self.matrix
         out = np.zeros((rows.size, cols.size))
         rr, cc = rows < lay.m, cols < lay.m
         out[np.ix_(rr, cc)] = a[np.ix_(rows[rr], cols[cc])]
@@ -169,6 +178,20 @@ class _WindowView(BlockProvider):
             if hit.size:
                 out[i, hit[0]] = 1.0
         return out
+
+
+def _augmented_run_view(prov, alpha: int, beta: int):
+    """run_view of an augmented provider (providers.py:338-402): the permuted
+    provider when l == 0, else the shifted-window view plus its finisher."""
+    lay = prov.layout
+    if lay.l == 0:
+        return permute_provider(prov, alpha, beta), None
+    if lay.k >= 5 and lay.l > 2 * lay.b:
+        raise BadPartitionError(
+            f"order {lay.m} with k={lay.k} needs {lay.l} padding indices, more than two blocks' worth "
+            f"({2 * lay.b}); use a partition with k <= 4 or one that divides the order more evenly")
+    rmap, cmap = window_maps(lay, alpha, beta)
+    return _WindowView(prov, rmap, cmap), window_finisher(lay, alpha, beta)
 
 
 RESIDENT_FRACTION = 0.5
@@ -197,7 +220,7 @@ def upload_rows(host: np.ndarray, device: int, chunk_bytes: int = 64 << 20):
     return dst
 
 
-class _MemoryProvider(BlockProvider):
+class _MemoryProvider(_MatrixElements, BlockProvider):
     """Blocks of an in-memory matrix (l = 0); host copy plus a lazily uploaded device copy."""
 
     def __init__(self, matrix, k: int):
@@ -245,15 +268,7 @@ class _MemoryProvider(BlockProvider):
         return out
 
     def run_view(self, alpha: int, beta: int):
-        lay = self.layout
-        if lay.l == 0:
-            return permute_provider(self, alpha, beta), None
-        if lay.k >= 5 and lay.l > 2 * lay.b:
-            raise BadPartitionError(
-                f"order {lay.m} with k={lay.k} needs {lay.l} padding indices, more than two blocks' worth "
-                f"({2 * lay.b}); use a partition with k <= 4 or one that divides the order more evenly")
-        rmap, cmap = window_maps(lay, alpha, beta)
-        return _WindowView(self, rmap, cmap), window_finisher(lay, alpha, beta)
+        return _augmented_run_view(self, alpha, beta)
 
     def _device_matrix(self, device: int):
         """M resident in HBM (uploaded once), or None when it would take more
@@ -325,6 +340,133 @@ class _FileProvider(_MemoryProvider):
 def make_file_provider(path, k: int) -> BlockProvider:
     """Provider over a BRIM file."""
     return _FileProvider(path, k)
+
+
+# --------------------------------------------------------------------------
+# LS-SVM kernel system matrix, generated on the device
+# --------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class KernelSpec:
+    """Gaussian-kernel system matrix of order n + 1 for n training inputs (providers.py:93-120).
+
+    Entry (1,1) is 0, the rest of the first row and column are 1, interior
+    (i, j) is exp(-||x_{i-1} - x_{j-1}||^2 / (2 sigma^2)) + delta_ij / gamma.
+    """
+
+    inputs: np.ndarray
+    gamma: float = 1.0
+    sigma: float = 1.0
+
+    def __post_init__(self):
+        x = np.ascontiguousarray(self.inputs, dtype=np.float64)
+        if x.ndim == 1:
+            x = x[:, None]
+        if x.ndim != 2 or x.shape[0] < 1 or x.shape[1] < 1:
+            raise DimensionMismatchError(f"kernel inputs must be (n, d), got {np.shape(self.inputs)}")
+        if not (self.gamma > 0) or not (self.sigma > 0):
+            raise BadPartitionError("kernel gamma and sigma must be positive")
+        x.setflags(write=False)
+        object.__setattr__(self, "inputs", x)
+
+    @property
+    def order(self) -> int:
+        return self.inputs.shape[0] + 1
+
+
+class KernelGenerator:
+    """Device-side state of a KernelSpec: the inputs (uploaded once per device)
+    and the two scalars exactly as the reference computes them
+    (`sq / (-2.0 * sigma**2)`, `+ 1.0 / gamma`, providers.py:192-198)."""
+
+    def __init__(self, spec: KernelSpec):
+        self.spec = spec
+        self.n, self.d = spec.inputs.shape
+        self.denom = -2.0 * spec.sigma ** 2
+        self.ridge = 1.0 / spec.gamma
+        self._dev = {}
+
+    def inputs_on(self, device: int):
+        t = self._dev.get(device)
+        if t is None:
+            import torch
+
+            t = torch.from_numpy(np.array(self.spec.inputs)).to(f"cuda:{device}")
+            self._dev[device] = t
+        return t
+
+
+def _generate_host(gen: KernelGenerator, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """Elements (rows x cols) of [[A, 0], [0, I]] computed on the device, returned to the host."""
+    import torch
+
+    from .device import Arena, current_device
+
+    dev = current_device()
+    nr, nc = rows.size, cols.size
+    n = max(nr, nc)
+    r = np.full(n, 2**31 - 1, dtype=np.int32)
+    c = np.full(n, 2**31 - 2, dtype=np.int32)
+    r[:nr], c[:nc] = rows, cols
+    rmap = torch.from_numpy(r).to(f"cuda:{dev}")
+    cmap = torch.from_numpy(c).to(f"cuda:{dev}")
+    with Arena(n, 1, device=dev) as ar:
+        ar.rbf(gen, [(0, 0, 0)], rmap, cmap)
+        return ar.view(0)[:nr, :nc].cpu().numpy()
+
+
+class _KernelProvider(BlockProvider):
+    """LS-SVM system matrix provider (providers.py:175-200, 479-482).
+
+    Nothing of order m is ever stored: every block the engine loads is
+    generated straight into its arena slot by `bri_rbf_blocks`, from the n x d
+    inputs held on the device.  Host fetches (`fetch_block`) go through the
+    same kernel.
+    """
+
+    def __init__(self, spec: KernelSpec, k: int):
+        self.spec = spec
+        self._gen = KernelGenerator(spec)
+        self.layout = BlockLayout.for_order(spec.order, k)
+
+    def _generator(self) -> KernelGenerator:
+        return self._gen
+
+    def _block(self, alpha: int, beta: int) -> np.ndarray:
+        b = self.layout.b
+        return _generate_host(self._gen, np.arange((alpha - 1) * b, alpha * b), np.arange((beta - 1) * b, beta * b))
+
+    def _elements(self, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+        return _generate_host(self._gen, rows, cols)
+
+    def run_view(self, alpha: int, beta: int):
+        return _augmented_run_view(self, alpha, beta)
+
+
+def make_kernel_provider(spec: KernelSpec, k: int) -> BlockProvider:
+    """Provider over a kernel system matrix, blocks generated on the device."""
+    return _KernelProvider(spec, k)
+
+
+def kernel_matrix(spec: KernelSpec) -> np.ndarray:
+    """The whole order-(n+1) kernel system matrix, generated on the device (providers.py:485-487)."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    from .device import current_device, stream_handle
+
+    dev = current_device()
+    gen = KernelGenerator(spec)
+    m = spec.order
+    out = torch.empty((m, m), dtype=torch.float64, device=f"cuda:{dev}")
+    lib = _native.load_library()
+    _native.context(dev)
+    x = gen.inputs_on(dev)
+    _native.check(lib.bri_rbf_dense(stream_handle(dev), ctypes.c_void_p(x.data_ptr()), gen.n, gen.d, gen.denom,
+                                    gen.ridge, ctypes.c_void_p(out.data_ptr()), m), "bri_rbf_dense")
+    return out.cpu().numpy()
 
 
 def permute_provider(provider: BlockProvider, alpha: int, beta: int) -> BlockProvider:

@@ -124,7 +124,22 @@ def main():
         arrays[f"pad_m{m}_k{k}_inverse"] = sink.finalize().copy()
         meta["padded"].append([m, k, seed])
 
-    # 9. exact operation counts k=2..7 (pkg/tests/test_instrumentation.py:42-50)
+    # 9. LS-SVM kernel system (providers.py:93-120,175-200; pkg/tests/test_providers.py:100-136,
+    #    test_acceptance.py:195-205): full matrices, a padded layout and full inverses
+    meta["kernel"] = []
+    for name, n, d, gamma, sigma, seed, k in (("k63", 63, 3, 1.0, 1.0, 63, 4), ("k5", 5, 3, 1.5, 0.8, 32, 2),
+                                              ("k40", 40, 9, 2.0, 1.3, 7, 4), ("k150", 150, 200, 0.5, 9.0, 8, 3)):
+        x = rng(seed).standard_normal((n, d))
+        spec = bri.KernelSpec(inputs=x, gamma=gamma, sigma=sigma)
+        arrays[f"kern_{name}_inputs"] = x
+        arrays[f"kern_{name}_matrix"] = bri.kernel_matrix(spec)
+        prov = bri.make_kernel_provider(spec, k)
+        sink = bri.MemorySink(prov.layout)
+        bri.invert_full(prov, sink)
+        arrays[f"kern_{name}_inverse"] = sink.finalize().copy()
+        meta["kernel"].append([name, n, d, gamma, sigma, k])
+
+    # 10. exact operation counts k=2..7 (pkg/tests/test_instrumentation.py:42-50)
     meta["counts"] = {str(k): [c.block_inversions, c.block_multiplications, c.block_subtractions,
                                c.schur_nodes] for k in range(2, 8) for c in [bri.predicted_counts(k)]}
 

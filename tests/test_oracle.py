@@ -96,3 +96,13 @@ def test_counts(golden):
         c = {"nodes": 0, "executed": 0}
         orc.invert_block(shifted(k, 82), k, 1, 1, counters=c)
         assert c["nodes"] == nodes and c["executed"] == nodes
+
+
+def test_kernel_matrix_oracle_matches_reference(golden):
+    """The oracle's LS-SVM element rule reproduces the reference's kernel_matrix bit for bit."""
+    from oracle import bri_oracle as orc
+
+    data, meta = golden
+    for name, n, d, gamma, sigma, k in meta["kernel"]:
+        got = orc.kernel_matrix(data[f"kern_{name}_inputs"], gamma, sigma)
+        np.testing.assert_array_equal(got, data[f"kern_{name}_matrix"])
