@@ -610,6 +610,9 @@ int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, in
                     int* status) {
   if (ar == nullptr || slots == nullptr || count < 0) return fail_msg("bri_getrf_batch: bad arguments");
   if (count == 0) return 0;
+  if (ar->v.n > max_panel_rows())
+    return fail_msg("bri_getrf_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
+                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   std::vector<int> h(7 * (size_t)count);
@@ -655,6 +658,9 @@ int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, co
 int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_invert_batch: bad arguments");
   if (count == 0) return 0;
+  if (ar->v.n > max_panel_rows())
+    return fail_msg("bri_invert_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
+                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   if (n <= SMALL_MAX) {
@@ -718,6 +724,9 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
 int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_schur_batch: bad arguments");
   if (count == 0) return 0;
+  if (ar->v.n > max_panel_rows())
+    return fail_msg("bri_schur_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
+                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   auto I = [&](int i, int k) { return items[7 * i + k]; };  // p, rt, l, r, out, f, w

@@ -29,7 +29,8 @@ namespace bri {
 
 namespace {
 
-constexpr int MAXCS = 8;            // cluster size cap (portable)
+constexpr int PORTABLE_CS = 8;      // preferred cluster size cap (portable)
+constexpr int MAXCS = 16;           // non-portable clusters for panels taller than 8 x 2 x PT rows
 
 // ----------------------------------------------------------------- maxabs
 // max |X| per slot (the scale of the singularity test, core.py:200-209).  One
@@ -641,17 +642,22 @@ cudaError_t configure_lu() {
   cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
+
+int max_panel_rows() { return MAXCS * 2 * PT; }
 
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                          const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
   const int h = a.n - j0;
   // 1 row per thread while it fits a cluster of 8, else 2 (registers: 2 x 32 doubles)
-  const int rpt = h <= MAXCS * PT ? 1 : 2;  // measured: 1 row/thread beats a halved cluster
+  // Up to 8 x PT rows: 1 row per thread, portable clusters (measured: beats a
+  // halved cluster at 2 rows); up to 8 x 2 x PT: 2 rows; beyond, 16-CTA clusters.
+  const int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
   int cs = 1;
   while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
-  if ((h + cs - 1) / cs > rpt * PT) return cudaErrorInvalidValue;  // n > 4096: TODO wider clusters
+  if ((h + cs - 1) / cs > rpt * PT) return cudaErrorInvalidValue;  // order > max_panel_rows()
   PanelArgs p;
   p.a = a;
   p.slots = slots;

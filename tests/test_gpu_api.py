@@ -278,3 +278,59 @@ def test_kernel_provider_inversion_matches_reference(bri, golden):
         mem = bri.MemorySink(prov.layout)
         bri.invert_full(bri.make_memory_provider(bri.kernel_matrix(spec), k), mem)
         np.testing.assert_array_equal(got, mem.finalize())
+
+
+def test_dense_lu_baseline_and_verify(bri, golden, tmp_path):
+    """GPU dense-LU path (baseline.py:27-88) and `bri verify` as a call (cli.py:261-296)."""
+    from paper_1612_00001_b200 import baseline
+
+    data, _ = golden
+    h = 1.0 / (np.arange(4)[:, None] + np.arange(4)[None, :] + 1.0)
+    assert rel_err(baseline.lu_invert_full(h), data["hilbert4_inv"]) <= 1e-10
+    for n in (1, 5, 12, 33, 64, 100):
+        x = data[f"inv{n}_matrix"]
+        out = baseline.lu_invert_full(x)
+        assert rel_err(out, data[f"inv{n}_out"]) <= 1e-13
+        np.testing.assert_array_equal(x, data[f"inv{n}_matrix"])  # input left intact
+    sing = np.ones((5, 5))
+    with pytest.raises(bri.SingularMatrixError):
+        baseline.lu_invert_full(sing)
+    with pytest.raises(bri.DimensionMismatchError):
+        baseline.lu_invert_full(np.zeros((2, 3)))
+    inv, rec = baseline.bench_lu(shifted(64, 3), seed=3)
+    assert rec.method == "lu" and rec.peak_bytes == 3 * 8 * 64 * 64
+    # materialize (trim / padded working matrix with its identity corner)
+    a = shifted(10, 88)
+    prov = bri.make_memory_provider(a, 4)
+    np.testing.assert_array_equal(baseline.materialize(prov), a)
+    full = baseline.materialize(prov, trim=False)
+    assert full.shape == (12, 12) and (full[10:, 10:] == np.eye(2)).all() and (full[:10, 10:] == 0).all()
+    with pytest.raises(bri.MaterializeLimitError):
+        baseline.materialize(prov, limit=8)
+    # verify: computed candidate, BRIM candidate, mismatched order, and a failing candidate
+    rep = baseline.verify(a, k=4)
+    assert rep["pass"] and rep["m"] == 10 and rep["max_rel_error"] <= 1e-8
+    src, good = tmp_path / "a.brim", tmp_path / "inv.brim"
+    bri.write_matrix(src, a)
+    bri.write_matrix(good, baseline.lu_invert_full(a))
+    assert baseline.verify(src, inverse=good)["max_rel_error"] == 0.0
+    bad = baseline.lu_invert_full(a)
+    bad[3, 4] += 1.0
+    rep = baseline.verify(a, inverse=bad)
+    assert not rep["pass"] and rep["at"] == [3, 4]
+    with pytest.raises(bri.UsageError):
+        baseline.verify(a, inverse=np.eye(3))
+
+
+@pytest.mark.parametrize("n", [4097, 6144, 8192])
+def test_dense_inverse_tall_panels(bri, n):
+    """Orders above 4096 factor their panels on 16-CTA (non-portable) clusters."""
+    import torch
+
+    from paper_1612_00001_b200 import baseline
+
+    a = shifted(n, n)
+    inv = baseline.lu_invert_full(a)
+    ta, ti = torch.from_numpy(a).cuda(), torch.from_numpy(inv).cuda()
+    res = (ta @ ti - torch.eye(n, dtype=torch.float64, device="cuda")).abs().max().item()
+    assert res <= 1e-12, res
