@@ -163,6 +163,12 @@ BRI_DEVI void st_async_f64(uint32_t addr, double v, uint32_t mbar) {
                : "memory");
 }
 
+BRI_DEVI void st_async_v2_f64(uint32_t addr, double a, double b, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(mbar)
+               : "memory");
+}
+
 BRI_DEVI void st_async_s32(uint32_t addr, int v, uint32_t mbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
                "r"(mbar)

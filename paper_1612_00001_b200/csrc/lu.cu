@@ -109,40 +109,50 @@ __global__ void pi_init_kernel(int* pi, int n) {
 
 // ------------------------------------------------------------------ panel
 // The (n - j0) x nb panel (nb <= 32) is spread over a cluster of cs CTAs of
-// PT threads; thread t of CTA r owns rows row_lo + q*PT + t (q < RPT) and keeps
-// their not-yet-final values in registers, *shifted*: after column jj,
-// x[q][c] holds column jj+1+c.  The shift keeps every register index static
-// while the column loop stays rolled (a fully unrolled panel overflowed the
-// instruction cache: 46% no_instruction stalls).  Finished values — the
-// multipliers (L) of every row and the U rows of the pivots — live in shared
-// memory psm[c * rhp + i] and are written back at the end.  Row buffers are
-// 64 wide with a zero upper half, so shifted reads need no predicates.
+// PT threads.  Thread t of CTA r owns the *slots* row_lo + q*PT + t (q < RPT):
+// a slot is one original row of the panel, and its data never moves.  The
+// not-yet-final values live in registers, *shifted*: after column jj, x[q][c]
+// holds column jj+1+c (static register indices while the column loop stays
+// rolled — a fully unrolled panel overflowed the instruction cache).  Each
+// slot carries its current row position pos[q]; an interchange of rows j and
+// p just exchanges two positions ("lazy relocation"), so no row ever travels
+// between CTAs and the only data a column exchanges is the pivot candidates.
+// Finished values — the multipliers (L) of every slot and the U rows of the
+// pivots — live in shared memory psm[c * rhp + slot]; at the end every slot
+// is written to its final position.
 // Per column jj (pivot position j = j0 + jj):
-//   (1) thread candidate, warp shuffle argmax; each warp's winning lane
-//       stores its row (L part from psm by the lanes, live part from its
-//       registers) to wrow[warp]; the owner of row j stores row j -> barrier
-//   (2) every thread picks the CTA winner from the PW slots
-//   (3) cs > 1: warp 0 pushes the CTA candidate row to every CTA (DSMEM),
-//       warp 1 of row j's owner pushes row j -> cluster barrier
-//   (4) every thread picks the global winner; rows j and p are exchanged
-//       (pivot row final in psm); active rows scale and rank-1 update (31 DFMA).
+//   (1) the CTA winner (largest |x|, smallest position on ties; NaNs never
+//       win) from the per-warp slots written at the end of the previous column
+//   (2) its owning thread stages the live row + (value, position) as one
+//       288-byte message; cs > 1: the message is bulk-copied into slot `rank`
+//       of every CTA of the cluster, completing on their exchange mbarrier
+//   (3) every thread picks the global winner p from the cs candidates: the
+//       pivot row (u) is read straight from the winning message
+//   (4) positions j and p are exchanged (the finished pivot stores its U row),
+//       active slots scale, form the next column first, reduce the next
+//       candidate, then finish the rank-1 update (31 DFMA per slot).
+// Pivot decisions are dgetf2's: idamax (first index on ties), interchange
+// only for a nonzero pivot, reciprocal scaling when |pivot| >= sfmin; a
+// column without any comparable value (all NaN) pivots in place.
 #ifdef BRI_PANEL_PROFILE
-__device__ unsigned long long g_panel_phase[8];
+__device__ unsigned long long g_panel_phase[10];
 #define PPROF(k)                                                         \
   do {                                                                   \
     if (threadIdx.x == 0 && blockIdx.x == 0) {                           \
       const unsigned long long now = clock64();                          \
-      g_panel_phase[k] += now - t_last;                                  \
+      ph_acc[k] += now - t_last;                                         \
       t_last = now;                                                      \
     }                                                                    \
   } while (0)
 #else
 #define PPROF(k) do { } while (0)
 #endif
+#ifndef BRI_PANEL_BULK
+#define BRI_PANEL_BULK 0
+#endif
 constexpr int PT = 256;
 constexpr int PW = PT / 32;
 constexpr int PNB = NBMAX;      // live register width (narrower panels are zero-padded)
-constexpr int RW = 2 * PNB;     // row buffer width (upper half zero)
 
 struct PanelArgs {
   ArenaView a;
@@ -154,9 +164,8 @@ struct PanelArgs {
   int n_stride, pair_stride;
 };
 
-
-// The owning lane stores its live row, shifted (x[c] -> dst[c + 1]), with
-// 16-byte stores; dst is a 16-byte aligned 34-wide buffer (tail stays zero).
+// Live row of slot q, shifted (x[c] -> dst[c + 1]), with 16-byte stores; dst
+// is a 16-byte aligned 34-wide buffer whose ends stay zero.
 template <int RPT>
 BRI_DEVI void store_live_row(double* dst, const double (&x)[RPT][PNB], int q) {
   double r[PNB];
@@ -173,27 +182,29 @@ BRI_DEVI void store_live_row(double* dst, const double (&x)[RPT][PNB], int q) {
   dst[PNB] = r[PNB - 1];
 }
 
+// The U row of a slot that just became pivot j0 + jj: its live values are
+// columns jj.. of the panel.
+BRI_DEVI void store_u_row(double* psm, int rhp, int jj, int nb, int slot, const double (&xr)[PNB]) {
+#pragma unroll
+  for (int c = 0; c < PNB; ++c)
+    if (jj + c < nb) psm[(jj + c) * rhp + slot] = xr[c];
+}
+
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
-  // Row buffers are split: L part (columns < jj) and the live part in
-  // *shifted* coordinates, x[c] (column jj + c) stored at index c + 1 of a
-  // 34-wide buffer whose tail is zero, so the update reads u[c] = buf[c + 2]
-  // with aligned 16-byte loads.
   constexpr int SW = 34;
-  // one 544-byte message per row: L part, shifted live part, (value, row, origin)
-  struct __align__(16) RowMsg {
-    double L[PNB];
+  // one 288-byte message per CTA candidate: shifted live row, value, position
+  struct __align__(16) CandMsg {
     double S[SW];
     double val;
-    int idx, orig;
+    int pos, pad;
   };
-  static_assert(sizeof(RowMsg) % 16 == 0, "bulk copies move 16-byte multiples");
-  extern __shared__ double psm[];                       // nb columns x rhp rows, then rhp ints
+  static_assert(sizeof(CandMsg) % 16 == 0, "bulk copies move 16-byte multiples");
+  extern __shared__ double psm[];                       // nb columns x rhp slots, then rhp ints
   __shared__ double wval[2][PW];
-  __shared__ int widx[2][PW];
-  __shared__ RowMsg cmsg[2][MAXCS];                     // candidates, by source CTA rank
-  __shared__ RowMsg jmsg[2];                            // row j, from its owner CTA
-  __shared__ RowMsg cstg[2], jstg[2];                   // local staging of outgoing messages (cs > 1)
+  __shared__ int wpos[2][PW];
+  __shared__ CandMsg cmsg[2][MAXCS];                    // candidates, by source CTA rank
+  __shared__ CandMsg cstg[2];                           // local staging of the outgoing message (cs > 1)
   __shared__ __align__(8) uint64_t xbar[2];             // exchange mbarriers (cs > 1)
 
   const int cs = (int)cluster_nctarank();
@@ -201,19 +212,15 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   const int item = blockIdx.x / cs;
   const int n = p.a.n, ld = p.a.ld, nb = p.nb, j0 = p.j0, rhp = p.rhp;
   double* X = p.a.base + (long long)p.slots[item] * p.a.slot_elems;
-  int* orig = reinterpret_cast<int*>(psm + (long long)nb * rhp);
+  int* fpos = reinterpret_cast<int*>(psm + (long long)nb * rhp);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row_lo = j0 + rank * p.rows_per_cta;
   const int myrows = max(0, min(n, row_lo + p.rows_per_cta) - row_lo);
-  // bytes each CTA receives per column: cs candidates + row j
-  const uint32_t xbytes = (uint32_t)(cs + 1) * (uint32_t)sizeof(RowMsg);
+  const uint32_t xbytes = (uint32_t)cs * (uint32_t)sizeof(CandMsg);
+  const double kNaN = __longlong_as_double(0x7ff8000000000000LL);
 
   for (int e = tid; e < 2 * MAXCS * SW; e += PT) cmsg[e / (MAXCS * SW)][(e / SW) % MAXCS].S[e % SW] = 0.0;
-  for (int e = tid; e < 2 * SW; e += PT) {
-    jmsg[e / SW].S[e % SW] = 0.0;
-    cstg[e / SW].S[e % SW] = 0.0;
-    jstg[e / SW].S[e % SW] = 0.0;
-  }
+  for (int e = tid; e < 2 * SW; e += PT) cstg[e / SW].S[e % SW] = 0.0;
   if (tid == 0) {
     mbar_init(&xbar[0], 1);
     mbar_init(&xbar[1], 1);
@@ -221,35 +228,35 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
   }
 
   double x[RPT][PNB];
-  int gi[RPT];
+  int pos[RPT];
   bool valid[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
     const int li = q * PT + tid;
-    gi[q] = row_lo + li;
+    pos[q] = row_lo + li;
     valid[q] = li < myrows;
 #pragma unroll
     for (int c = 0; c < PNB; ++c)
-      x[q][c] = (valid[q] && c < nb) ? X[gi[q] + (long long)(j0 + c) * ld] : 0.0;
-    if (valid[q]) orig[li] = gi[q];
+      x[q][c] = (valid[q] && c < nb) ? X[pos[q] + (long long)(j0 + c) * ld] : 0.0;
   }
-  // candidate for column 0
+  // candidate for column 0 (every slot is active)
   double bv = -1.0;
-  int bi = INT_MAX, bq = 0;
+  int bp = INT_MAX;
 #pragma unroll
   for (int q = 0; q < RPT; ++q)
     if (valid[q]) {
       const double v = fabs(x[q][0]);
-      if (v > bv || (v == bv && gi[q] < bi)) { bv = v; bi = gi[q]; bq = q; }
+      if (v > bv || (v == bv && pos[q] < bp)) { bv = v; bp = pos[q]; }
     }
   {
     double wv = bv;
-    int wi = bi;
+    int wi = bp;
     warp_argmax_fast(wv, wi);
-    if (lane == 0) { wval[0][warp] = wv; widx[0][warp] = wi; }
+    if (lane == 0) { wval[0][warp] = wv; wpos[0][warp] = wi; }
   }
   if (cs > 1) cluster_sync_all(); else __syncthreads();
 #ifdef BRI_PANEL_PROFILE
+  unsigned long long ph_acc[10] = {0};
   unsigned long long t_last = clock64();
 #endif
 
@@ -257,128 +264,103 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     const int j = j0 + jj;
     const int par = jj & 1;
     if (cs > 1 && tid == 0) mbar_arrive_expect_tx(&xbar[par], xbytes);
-    // ---- (2) CTA winner from the warp slots (written at the end of the previous column)
+    // ---- (1) CTA winner from the warp slots
     double cv = wval[par][lane % PW];
-    int ci = widx[par][lane % PW];
-    warp_argmax_fast(cv, ci);
+    int cp = wpos[par][lane % PW];
+    warp_argmax_fast(cv, cp);
     PPROF(0);
-    // ---- (3) publish: the CTA winner's row and row j, by their owning warps
-    const bool have = ci != INT_MAX;
-    const int lw = ci - row_lo;                    // local index of the CTA winner
-    const bool own_j = (j >= row_lo && j < row_lo + myrows);
-    const int lj = j - row_lo;
-    uint32_t aL, aS, bL, bS;
-    int pr, uorig, jorig;
+    // ---- (2) stage the CTA candidate; cs > 1: push it to every CTA
+    CandMsg* out = cs > 1 ? &cstg[par] : &cmsg[par][0];
+    bool mine = false;
+    int mq = 0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+      if (valid[q] && pos[q] == cp) { mine = true; mq = q; }
+    if (mine) {
+      store_live_row<RPT>(out->S, x, mq);
+      out->val = cv;
+      out->pos = cp;
+    } else if (cp == INT_MAX && tid == 0) {
+      out->val = -1.0;
+      out->pos = INT_MAX;
+    }
+    int gp;
+    const CandMsg* win;
     if (cs > 1) {
-      // stage our CTA candidate (and row j if we own it) as one message each,
-      // then one lane bulk-copies it into slot `rank` of every CTA of the cluster
-      if (have && warp == ((lw % PT) >> 5)) {
-        if (lane == (lw & 31)) {
-          store_live_row<RPT>(cstg[par].S, x, lw / PT);
-          cstg[par].val = cv;
-          cstg[par].idx = ci;
-          cstg[par].orig = orig[lw];
-        }
-        cstg[par].L[lane] = lane < jj ? psm[lane * rhp + lw] : 0.0;
-      } else if (!have && warp == 0) {
-        cstg[par].L[lane] = 0.0;
-        if (lane == 0) {
-          cstg[par].val = -1.0;
-          cstg[par].idx = INT_MAX;
-          cstg[par].orig = -1;
-        }
-      }
-      if (own_j && warp == ((lj % PT) >> 5)) {
-        if (lane == (lj & 31)) {
-          store_live_row<RPT>(jstg[par].S, x, lj / PT);
-          jstg[par].orig = orig[lj];
-        }
-        jstg[par].L[lane] = lane < jj ? psm[lane * rhp + lj] : 0.0;
-      }
-      const bool pub_c = (have && warp == ((lw % PT) >> 5)) || (!have && warp == 0);
-      const bool pub_j = own_j && warp == ((lj % PT) >> 5);
-      if (pub_c || pub_j) {
+      const bool pub = __any_sync(0xffffffffu, mine) || (cp == INT_MAX && warp == 0);
+      if (pub) {
+#if BRI_PANEL_BULK
         fence_proxy_async_smem();   // generic smem writes -> visible to the bulk-copy engine
         __syncwarp();
-        // one destination per lane: the bulk copies are issued in parallel
-        if (pub_c && lane < cs)
-          bulk_s2cluster(dsmem_addr(&cmsg[par][rank], lane), &cstg[par], sizeof(RowMsg), dsmem_addr(&xbar[par], lane));
-        if (pub_j && lane >= 16 && lane < 16 + cs)
-          bulk_s2cluster(dsmem_addr(&jmsg[par], lane - 16), &jstg[par], sizeof(RowMsg),
-                         dsmem_addr(&xbar[par], lane - 16));
+        if (lane < cs)
+          bulk_s2cluster(dsmem_addr(&cmsg[par][rank], lane), out, sizeof(CandMsg), dsmem_addr(&xbar[par], lane));
+#else
+        // 18 16-byte chunks per destination, (chunk, destination) pairs spread
+        // over the warp's lanes; each st.async completes on the peer's mbarrier
+        __syncwarp();
+        constexpr int CH = (int)(sizeof(CandMsg) / 16);
+        const uint32_t src = smem_u32(out);
+        for (int k = lane; k < CH * cs; k += 32) {
+          const int e = k % CH, d = k / CH;
+          double c0, c1;
+          lds_f64x2(src + 16 * e, c0, c1);
+          st_async_v2_f64(dsmem_addr(&cmsg[par][rank], d) + 16 * e, c0, c1, dsmem_addr(&xbar[par], d));
+        }
+#endif
       }
       PPROF(1);
       mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);
       PPROF(2);
+      // ---- (3) global winner
       double gv = lane < cs ? cmsg[par][lane].val : -1.0;
-      int gidx = lane < cs ? cmsg[par][lane].idx : INT_MAX;
-      const int myidx = gidx;
-      warp_argmax_fast(gv, gidx);
-      const int gr = __ffs(__ballot_sync(0xffffffffu, lane < cs && gidx != INT_MAX && myidx == gidx)) - 1;
-      const bool none = gidx == INT_MAX;  // all NaN: idamax returns the first index
-      pr = none ? j : gidx;
-      aL = none ? smem_u32(jmsg[par].L) : smem_u32(cmsg[par][gr].L);
-      aS = none ? smem_u32(jmsg[par].S) : smem_u32(cmsg[par][gr].S);
-      uorig = none ? jmsg[par].orig : cmsg[par][gr].orig;
-      jorig = jmsg[par].orig;
+      gp = lane < cs ? cmsg[par][lane].pos : INT_MAX;
+      const int mypos = gp;
+      warp_argmax_fast(gv, gp);
+      const int gr = __ffs(__ballot_sync(0xffffffffu, lane < cs && gp != INT_MAX && mypos == gp)) - 1;
+      win = &cmsg[par][gr < 0 ? 0 : gr];
     } else {
-      if (have && warp == ((lw % PT) >> 5)) {
-        if (lane == (lw & 31)) {
-          store_live_row<RPT>(cmsg[par][0].S, x, lw / PT);
-          cmsg[par][0].orig = orig[lw];
-        }
-        if (lane < jj) cmsg[par][0].L[lane] = psm[lane * rhp + lw];
-      }
-      if (own_j && warp == ((lj % PT) >> 5)) {
-        if (lane == (lj & 31)) {
-          store_live_row<RPT>(jmsg[par].S, x, lj / PT);
-          jmsg[par].orig = orig[lj];
-        }
-        if (lane < jj) jmsg[par].L[lane] = psm[lane * rhp + lj];
-      }
       PPROF(1);
       __syncthreads();
       PPROF(2);
-      pr = have ? ci : j;
-      aL = have ? smem_u32(cmsg[par][0].L) : smem_u32(jmsg[par].L);
-      aS = have ? smem_u32(cmsg[par][0].S) : smem_u32(jmsg[par].S);
-      uorig = have ? cmsg[par][0].orig : jmsg[par].orig;
-      jorig = jmsg[par].orig;
+      gp = cp;
+      win = &cmsg[par][0];
     }
-    bL = smem_u32(jmsg[par].L);
-    bS = smem_u32(jmsg[par].S);
     PPROF(3);
-    // ---- (4) interchange, scale, rank-1 update; the next column's candidate
-    //          is formed as soon as its values are updated
-    const double piv = lds_f64(aS + 8);
+    // ---- (4) interchange, scale, rank-1 update
+    const bool none = gp == INT_MAX;      // no comparable value in the column: pivot in place
+    const int pr = none ? j : gp;
+    const uint32_t aS = smem_u32(win->S);
+    const double piv = none ? kNaN : lds_f64(aS + 8);
     if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
     const bool swap = (pr != j && piv != 0.0);  // dgetf2 interchanges only for a nonzero pivot
     const bool recip = fabs(piv) >= kSfmin;
     const double rinv = 1.0 / piv;
-    if (own_j && warp == ((lj % PT) >> 5)) {    // position j: the pivot row, final
-      const uint32_t sL = swap ? aL : bL, sS = swap ? aS : bS;
-      if (lane < nb) psm[lane * rhp + lj] = lane < jj ? lds_f64(sL + 8 * lane) : lds_f64(sS + 8 * (lane - jj + 1));
-      if (lane == 0 && swap) orig[lj] = uorig;
-    }
-    const bool own_p = swap && pr >= row_lo && pr < row_lo + myrows;
-    const int lp = pr - row_lo;
-    if (own_p && warp == ((lp % PT) >> 5)) {    // position p: old row j's L part
-      if (lane < jj) psm[lane * rhp + lp] = lds_f64(bL + 8 * lane);
-      if (lane == 0) orig[lp] = jorig;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      if (!valid[q]) continue;
+      bool fin = false;
+      if (pos[q] == j) {
+        if (swap) pos[q] = pr; else fin = true;
+      } else if (swap && pos[q] == pr) {
+        pos[q] = j;
+        fin = true;
+      }
+      if (fin) store_u_row(psm, rhp, jj, nb, q * PT + tid, x[q]);
     }
     PPROF(4);
     double u[PNB];
+    if (none) {
 #pragma unroll
-    for (int c = 0; c < PNB; c += 2) lds_f64x2(aS + 16 + 8 * c, u[c], u[c + 1]);
+      for (int c = 0; c < PNB; ++c) u[c] = kNaN;
+    } else {
+#pragma unroll
+      for (int c = 0; c < PNB; c += 2) lds_f64x2(aS + 16 + 8 * c, u[c], u[c + 1]);
+    }
     double nl[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       nl[q] = 0.0;
-      if (!valid[q] || gi[q] <= j) continue;
-      if (own_p && gi[q] == pr) {
-#pragma unroll
-        for (int c = 0; c < PNB; ++c) x[q][c] = lds_f64(bS + 8 * (c + 1));
-      }
+      if (!valid[q] || pos[q] <= j) continue;
       double l = x[q][0];
       if (piv != 0.0) l = recip ? l * rinv : l / piv;
       nl[q] = l;
@@ -387,50 +369,60 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     }
     // next column's candidate + warp reduction (overlaps the remaining updates)
     bv = -1.0;
-    bi = INT_MAX;
+    bp = INT_MAX;
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
-      if (valid[q] && gi[q] > j) {
+      if (valid[q] && pos[q] > j) {
         const double v = fabs(x[q][0]);
-        if (v > bv || (v == bv && gi[q] < bi)) { bv = v; bi = gi[q]; bq = q; }
+        if (v > bv || (v == bv && pos[q] < bp)) { bv = v; bp = pos[q]; }
       }
     {
       double wv = bv;
-      int wi = bi;
+      int wi = bp;
       warp_argmax_fast(wv, wi);
-      if (lane == 0) { wval[par ^ 1][warp] = wv; widx[par ^ 1][warp] = wi; }
+      if (lane == 0) { wval[par ^ 1][warp] = wv; wpos[par ^ 1][warp] = wi; }
     }
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-      if (!valid[q] || gi[q] <= j) continue;
+      if (!valid[q] || pos[q] <= j) continue;
 #pragma unroll
       for (int c = 1; c < PNB - 1; ++c) x[q][c] = fma(-nl[q], u[c], x[q][c + 1]);
       x[q][PNB - 1] = 0.0;
     }
     PPROF(5);
-    __syncthreads();   // warp slots of the next column complete; rows j/p settled
+    __syncthreads();   // warp slots of the next column complete
   }
+#ifdef BRI_PANEL_PROFILE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    for (int k = 0; k < 10; ++k) atomicAdd(&g_panel_phase[k], ph_acc[k]);
+#endif
 
-  // write back; publish the interchange map for the rowpanel kernel
+  // write every slot to its final position; publish the interchange map for
+  // the rowpanel kernel (position P now holds original row g)
+#pragma unroll
+  for (int q = 0; q < RPT; ++q)
+    if (valid[q]) fpos[q * PT + tid] = pos[q];
+  __syncthreads();
   for (int e = tid; e < nb * myrows; e += PT) {
     const int c = e / myrows, i = e % myrows;
-    X[(row_lo + i) + (long long)(j0 + c) * ld] = psm[c * rhp + i];
+    X[fpos[i] + (long long)(j0 + c) * ld] = psm[c * rhp + i];
   }
   int* sig = p.sigma + (long long)item * p.n_stride;
   int* pairs = p.pairs + (long long)item * p.pair_stride + (long long)p.pidx * (1 + 2 * NBMAX);
   for (int i = tid; i < myrows; i += PT) {
-    const int g = row_lo + i, o = orig[i];
-    if (g < j0 + nb) {
-      sig[g] = o;
-    } else if (o != g) {
+    const int P = fpos[i], g = row_lo + i;
+    if (P < j0 + nb) {
+      sig[P] = g;
+    } else if (P != g) {
       const int k = atomicAdd(pairs, 1);
-      pairs[1 + 2 * k] = g;
-      pairs[2 + 2 * k] = o;
+      pairs[1 + 2 * k] = P;
+      pairs[2 + 2 * k] = g;
     }
   }
   // no CTA may exit while a peer could still address its shared memory
   if (cs > 1) cluster_sync_all();
 }
+
 
 // --------------------------------------------------------------- rowpanel
 // One warp per X-column outside the panel (a contiguous memory row): apply
@@ -561,10 +553,12 @@ __global__ void diag_check_kernel(ArenaView a, const int* slots, const unsigned 
 
 }  // namespace
 
+
+
 #ifdef BRI_PANEL_PROFILE
 void panel_profile_read(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_panel_phase, sizeof(g_panel_phase));
-  unsigned long long z[8] = {0};
+  unsigned long long z[10] = {0};
   cudaMemcpyToSymbol(g_panel_phase, z, sizeof(z));
 }
 #endif

@@ -25,7 +25,7 @@ namespace {
 
 constexpr int T = TRSM_BLOCK;      // 64
 constexpr int BN = 32;             // right-hand-side columns per CTA
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;      // 3 stages keep two CTAs resident per SM (latency hiding across solves)
 constexpr int THREADS = 256;
 constexpr int STAGE_BYTES = StageGeom<T, BN>::BYTES;  // 12 KB
 constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
@@ -107,7 +107,7 @@ struct TrsmArgs {
 };
 
 template <bool LOWER>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS, 2)
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

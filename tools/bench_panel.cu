@@ -3,6 +3,7 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include "../paper_1612_00001_b200/csrc/bri_internal.h"
+namespace bri { void count_launch() {} }
 using namespace bri;
 int main() {
   configure_lu();

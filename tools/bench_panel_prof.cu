@@ -16,8 +16,8 @@ int main() {
   LuScratch sc;
   cudaMalloc(&sc.ipiv, n * 4); cudaMalloc(&sc.pi, n * 4); cudaMalloc(&sc.sigma, n * 4);
   cudaMalloc(&sc.pairs, 200 * 65 * 4); cudaMemset(sc.pairs, 0, 200 * 65 * 4);
-  unsigned long long ph[8];
-  for (int j0 : {0, 3840, 4000}) {
+  unsigned long long ph[10];
+  for (int j0 : {0, 1024, 2048, 3072, 3840, 4000}) {
     launch_panel(a, slots, 1, j0, 32, 0, sc, n, 65, 0);
     cudaDeviceSynchronize();
     panel_profile_read(ph);
@@ -25,8 +25,8 @@ int main() {
     cudaDeviceSynchronize();
     panel_profile_read(ph);
     printf("H=%d cycles/col:", n - j0);
-    const char* nm[6] = {"ctawinner", "publish", "wait", "select", "swap", "update+nextcand"};
-    for (int k = 0; k < 6; ++k) printf(" %s=%.0f", nm[k], ph[k] / 320.0);
+    const char* nm[9] = {"ctawinner", "bulkissue", "wait", "select", "swap", "update+nextcand", "stage_j", "fence", "stage_cand"};
+    for (int k = 0; k < 9; ++k) printf(" %s=%.0f", nm[k], ph[k] / 320.0);
     printf("  err=%s\n", cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
