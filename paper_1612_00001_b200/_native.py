@@ -14,7 +14,7 @@ import threading
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbri_b200.so")
+LIB_PATH = os.environ.get("BRI_LIB") or os.path.join(_HERE, "libbri_b200.so")
 
 # (name, restype, argtypes) — must match include/bri_b200.h
 _c_int, _c_void_p, _c_double, _c_ll = ctypes.c_int, ctypes.c_void_p, ctypes.c_double, ctypes.c_longlong

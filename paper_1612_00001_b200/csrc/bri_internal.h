@@ -42,9 +42,13 @@ struct GemmParams {
   int a_r0, a_c0, b_r0, b_c0, c_r0, c_c0;
   double alpha, beta;
   int tiles_m, tiles_n;
+  int count;      // batch size (set by launch_gemm)
+  int max_ctas;   // > 0: persistent launch with at most this many CTAs
 };
 
 int gemm_smem_bytes();
+int skinny_max_k();
+long long skinny_max_tiles();
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p,
                         int count, cudaStream_t stream);
 cudaError_t launch_scale_copy(const GemmParams& p, int count, cudaStream_t stream);

@@ -157,8 +157,10 @@ LuScratch lu_scratch(void* base, const LuLayout& L) {
 }
 
 int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, int M, int N, int K,
-              int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta) {
+              int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta,
+              int max_ctas = 0) {
   GemmParams p{};
+  p.max_ctas = max_ctas;
   p.base = ar->v.base;
   p.ld = ar->v.ld;
   p.slot_elems = ar->v.slot_elems;
@@ -220,11 +222,23 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     return 0;
   };
   // apply block J's interchanges / U12 solve / rank-W update to columns [c0, c1)
-  auto update_cols = [&](cudaStream_t st, int J0, int W, int pidx0, int c0, int c1) -> int {
+  // (cap > 0: the GEMM runs persistent on at most `cap` CTAs, leaving SMs to
+  // the critical path that factors the next block concurrently)
+  auto update_cols = [&](cudaStream_t st, int J0, int W, int pidx0, int c0, int c1, int cap) -> int {
     if (c1 <= c0) return 0;
     BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, v, dev_ff, count, dl, true, J0, W, c0, c1 - c0, false, st));
-    return gemm_call(ar, st, dev_ffff, count, n - J0 - W, c1 - c0, W, J0 + W, J0, J0, c0, J0 + W, c0, -1.0, 1.0);
+    return gemm_call(ar, st, dev_ffff, count, n - J0 - W, c1 - c0, W, J0 + W, J0, J0, c0, J0 + W, c0, -1.0, 1.0,
+                     cap);
   };
+  // Few factorizations in flight: their panel chain is the critical path and
+  // would otherwise wait for the trailing GEMM's CTAs to drain (measured on
+  // config 2: cap 80 -> 37.0 ms/step vs 39.4 uncapped).  Large batches keep
+  // every SM busy with panels of their own, so their updates run uncapped.
+  static const int trail_cap_env = [] {
+    const char* e = getenv("BRI_TRAIL_CAP");
+    return e ? atoi(e) : -1;
+  }();
+  const int trail_cap = trail_cap_env >= 0 ? trail_cap_env : (count <= 2 ? 80 : 0);
 
   const int npan_outer = outer / nbi;
   static const bool lookahead = [] {
@@ -242,7 +256,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N0, n, sc, n,
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
-      if (int rc = update_cols(s, J0, W, pidx0, N0, n)) return rc;
+      if (int rc = update_cols(s, J0, W, pidx0, N0, n, 0)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer)) return rc;
     } else if (WN > 0) {
       // critical path: next block's columns, then factor it
@@ -250,12 +264,12 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
       BRI_CHECK(cudaEventRecord(ctx->ev_a, s));
-      if (int rc = update_cols(s, J0, W, pidx0, N0, N0 + WN)) return rc;
+      if (int rc = update_cols(s, J0, W, pidx0, N0, N0 + WN, 0)) return rc;
       // bulk: everything else, concurrently on the side stream
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N0 + WN, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N0 + WN, n)) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N0 + WN, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer)) return rc;
       BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));

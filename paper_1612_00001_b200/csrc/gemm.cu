@@ -29,11 +29,16 @@
 #include "bri_internal.h"
 #include "dmma_tile.cuh"
 
+#include <cstdlib>
+
 namespace bri {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = TILE_BK, STAGES = 4;
+#ifndef BRI_GEMM_STAGES
+#define BRI_GEMM_STAGES 4
+#endif
+constexpr int BM = 128, BN = 128, BK = TILE_BK, STAGES = BRI_GEMM_STAGES;
 // 16 warps in a 4 x 4 grid, 32 x 32 warp tiles: four warps per scheduler hide
 // DMMA / LDS latency (8 warps of 64 x 32 tiles left the DMMA pipe ~80% busy).
 constexpr int WARPS_M = 4, WARPS_N = 4;
@@ -144,12 +149,236 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+
+// Persistent variant: tiles dealt round-robin over a capped grid (used when a
+// concurrent critical path must keep SMs, e.g. the LU's bulk trailing update).
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_persistent_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                           GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int KT = (p.K + BK - 1) / BK;
+  const int tiles_per_item = p.tiles_m * p.tiles_n;
+  const int total = tiles_per_item * p.count;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NUM_WARPS);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  // Producer: lane 0 of warp 0 keeps the ring STAGES-1 k-tiles ahead; the slot
+  // of k-tile kt is refilled (for kt + STAGES) once all warps released it.
+  const bool producer = (warp == 0 && lane == 0);
+  if (producer) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  const int wm0 = (warp % WARPS_M) * WTM;
+  const int wn0 = (warp / WARPS_M) * WTN;
+
+  // Tiles are dealt round-robin over the grid (one per CTA unless the launch
+  // caps the CTA count, e.g. to leave SMs to a concurrent critical path); the
+  // ring position g0 and its mbarrier phases run on across a CTA's tiles.
+  int g0 = 0;
+  for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const int item = tile / tiles_per_item, rem = tile % tiles_per_item;
+    const int* it = p.items + 4 * item;
+    const int sa = it[0], sb = it[1], sc_in = it[2], sc_out = it[3];
+    const int tm = rem % p.tiles_m;
+    const int tn = rem / p.tiles_m;
+    const int m0 = tm * BM, n0 = tn * BN;
+    auto issue = [&](int kt) {
+      const int s = (g0 + kt) % STAGES;
+      tile_issue<BM, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, sa,
+                         p.b_r0 + kt * BK, p.b_c0 + n0, sb);
+    };
+    if (producer) {
+      for (int kt = 0; kt < STAGES && kt < KT; ++kt) {
+        const int gg = g0 + kt;
+        if (gg >= STAGES) mbar_wait(&empty[gg % STAGES], ((gg / STAGES) - 1) & 1);
+        issue(kt);
+      }
+    }
+    WarpAcc<WTM / 16, WTN / 8> acc;
+    acc.zero();
+    for (int kt = 0; kt < KT; ++kt) {
+      const int gg = g0 + kt, s = gg % STAGES;
+      mbar_wait(&full[s], (gg / STAGES) & 1);
+      const uint8_t* sA = smem + s * STAGE_BYTES;
+      acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (producer && kt >= 1) {
+        const int kp = kt - 1;
+        if (kp + STAGES < KT) {
+          const int gp = g0 + kp;
+          mbar_wait(&empty[gp % STAGES], (gp / STAGES) & 1);
+          issue(kp + STAGES);
+        }
+      }
+    }
+    g0 += KT;
+
+    // ---------------------------------------------------------- epilogue
+    // Stage alpha*acc through smem, then stream whole columns (contiguous in
+    // memory): every warp access is one 256 B run, and the C_in loads of two
+    // columns are in flight together (C_in may alias C_out).
+    __syncthreads();
+    double* tile_s = reinterpret_cast<double*>(smem);
+    acc.to_smem(tile_s, LDT, wm0, wn0, lane, p.alpha);
+    __syncthreads();
+    double* cout = p.base + (long long)sc_out * p.slot_elems;
+    const double* cin = p.base + (long long)sc_in * p.slot_elems;
+    const bool read_c = p.beta != 0.0;
+    for (int c = warp; c < BN; c += 2 * NUM_WARPS) {
+      double v[2][4], old[2][4];
+      long long off[2][4];
+      bool ok[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int col = c + u * NUM_WARPS;
+        const int gcol = n0 + col;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int row = lane + 32 * q;
+          const int grow = m0 + row;
+          ok[u][q] = grow < p.M && gcol < p.N;
+          off[u][q] = (long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld;
+          v[u][q] = tile_s[col * LDT + row];
+          old[u][q] = (ok[u][q] && read_c) ? cin[off[u][q]] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (ok[u][q]) cout[off[u][q]] = read_c ? fma(p.beta, old[u][q], v[u][q]) : v[u][q];
+    }
+    // the next tile's TMA writes (async proxy) reuse this smem
+    fence_proxy_async_smem();
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ skinny
+// Short-K updates (K <= 128: the rank-32 / rank-128 updates inside the
+// blocked LU) on 64 x 64 tiles: four times the CTAs of a 128 x 128 tile, no
+// TMA pipeline to fill, operands staged in 32-wide k chunks with plain
+// coalesced loads.  The DMMA sequence per output element (k ascending in
+// m16n8k4 steps from a zero accumulator, then fma(beta, C_in, alpha * acc))
+// is the big kernel's, so both paths give bit-identical results.
+constexpr int SK_BM = 64, SK_BN = 64, SK_KC = 32;
+constexpr int SK_LDA = SK_BM + 8;   // As[k][m]: A fragments 2 wavefronts
+constexpr int SK_LDB = SK_KC + 4;   // Bs[n][k]: B fragments 2 wavefronts
+
+__global__ void __launch_bounds__(256) skinny_kernel(GemmParams p) {
+  __shared__ double As[SK_KC * SK_LDA];
+  __shared__ double Bs[SK_BN * SK_LDB];
+  const int* it = p.items + 4 * blockIdx.y;
+  const double* A = p.base + (long long)it[0] * p.slot_elems;
+  const double* B = p.base + (long long)it[1] * p.slot_elems;
+  const double* cin = p.base + (long long)it[2] * p.slot_elems;
+  double* cout = p.base + (long long)it[3] * p.slot_elems;
+  const int m0 = (blockIdx.x % p.tiles_m) * SK_BM, n0 = (blockIdx.x / p.tiles_m) * SK_BN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp & 1) * 32, wn0 = (warp >> 1) * 16;   // 2 x 4 warps, 32 x 16 each
+  double acc[2][2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+  for (int k0 = 0; k0 < p.K; k0 += SK_KC) {
+    // A chunk: SK_KC columns of 64 contiguous rows; B chunk: 64 columns of SK_KC contiguous k
+    for (int e = threadIdx.x; e < SK_KC * SK_BM; e += blockDim.x) {
+      const int kk = e / SK_BM, m = e % SK_BM;
+      const bool ok = m0 + m < p.M && k0 + kk < p.K;
+      As[kk * SK_LDA + m] = ok ? A[(long long)(p.a_r0 + m0 + m) + (long long)(p.a_c0 + k0 + kk) * p.ld] : 0.0;
+    }
+    for (int e = threadIdx.x; e < SK_BN * SK_KC; e += blockDim.x) {
+      const int n = e / SK_KC, kk = e % SK_KC;
+      const bool ok = n0 + n < p.N && k0 + kk < p.K;
+      Bs[n * SK_LDB + kk] = ok ? B[(long long)(p.b_r0 + k0 + kk) + (long long)(p.b_c0 + n0 + n) * p.ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SK_KC; kk += 4) {
+      double a[2][2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        a[i][0] = As[(kk + t) * SK_LDA + wm0 + 16 * i + g];
+        a[i][1] = As[(kk + t) * SK_LDA + wm0 + 16 * i + g + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = Bs[(wn0 + 8 * j + g) * SK_LDB + kk + t];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+    }
+    __syncthreads();
+  }
+  // all C_in loads first (C_in may alias C_out): one round trip, not sixteen
+  const bool read_c = p.beta != 0.0;
+  double old[2][2][4];
+  long long off[2][2][4];
+  bool ok[2][2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int row = m0 + wm0 + 16 * i + g + ((v >> 1) << 3);
+        const int col = n0 + wn0 + 8 * j + 2 * t + (v & 1);
+        ok[i][j][v] = row < p.M && col < p.N;
+        off[i][j][v] = (long long)(p.c_r0 + row) + (long long)(p.c_c0 + col) * p.ld;
+        old[i][j][v] = (ok[i][j][v] && read_c) ? cin[off[i][j][v]] : 0.0;
+      }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (ok[i][j][v]) {
+          const double val = p.alpha * acc[i][j][v];
+          cout[off[i][j][v]] = read_c ? fma(p.beta, old[i][j][v], val) : val;
+        }
+}
+
 }  // namespace
 
 int gemm_smem_bytes() { return SMEM_BYTES; }
 
+// Dispatch thresholds for the short-K kernel (env overrides for tuning runs).
+static int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return (s && *s) ? atoi(s) : dflt;
+}
+int skinny_max_k() {
+  static const int v = env_int("BRI_SKINNY_MAXK", 128);
+  return v;
+}
+long long skinny_max_tiles() {
+  static const long long v = env_int("BRI_SKINNY_MAXTILES", 148);   // 128x128 tiles (x batch) below one wave
+  return v;
+}
+
 cudaError_t configure_gemm() {
-  return cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  return e;
 }
 
 cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p0,
@@ -162,9 +391,24 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     // C_out = beta * C_in: handled by the scale kernel (no products)
     return launch_scale_copy(p, count, stream);
   }
-  dim3 grid(p.tiles_m * p.tiles_n, count);
+  if (p.K <= skinny_max_k() && (long long)p.tiles_m * p.tiles_n * count < skinny_max_tiles()) {
+    GemmParams q = p;
+    q.tiles_m = (p.M + SK_BM - 1) / SK_BM;
+    q.tiles_n = (p.N + SK_BN - 1) / SK_BN;
+    count_launch();
+    skinny_kernel<<<dim3(q.tiles_m * q.tiles_n, count), 256, 0, stream>>>(q);
+    return cudaGetLastError();
+  }
+  p.count = count;
+  long long ctas = (long long)p.tiles_m * p.tiles_n * count;
+  if (p.max_ctas > 0 && ctas > p.max_ctas) ctas = p.max_ctas;
+  if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   count_launch();
-  gemm_kernel<<<grid, THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+  if (ctas < (long long)p.tiles_m * p.tiles_n * count) {
+    gemm_persistent_kernel<<<dim3((unsigned)ctas), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+  } else {
+    gemm_kernel<<<dim3(p.tiles_m * p.tiles_n, count), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+  }
   return cudaGetLastError();
 }
 

@@ -21,4 +21,17 @@ with Arena(n, 4) as ar:
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         out[f"{M}x{N}x{K}"] = {"us": round(ms * 1000, 1), "tflops": round(2 * M * N * K / ms / 1e9, 2)}
+# a batched DAG level: 64 independent b=1024 Schur updates in one launch
+with Arena(1024, 4 * 64) as ar:
+    ar.tensor.normal_()
+    items = [(4 * i, 4 * i + 1, 4 * i + 2, 4 * i + 3) for i in range(64)]
+    for _ in range(2):
+        ar.gemm(items, 1024, 1024, 1024, alpha=-1.0, beta=1.0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        ar.gemm(items, 1024, 1024, 1024, alpha=-1.0, beta=1.0)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    out["64x1024^3"] = {"us": round(ms * 1000, 1), "tflops": round(64 * 2 * 1024**3 / ms / 1e9, 2)}
 print(json.dumps(out))
