@@ -6,6 +6,12 @@
 
 #include <cstdint>
 
+// A-operand TMA boxes: 16 x 16 doubles with 128-byte swizzle (1) or 8 x 16 with
+// 64-byte swizzle (0); the arena's tensor map and dmma_tile.cuh must agree.
+#ifndef BRI_WIDE_A
+#define BRI_WIDE_A 1
+#endif
+
 namespace bri {
 
 // Every kernel launch made by the library bumps this (exported as bri_launch_count).

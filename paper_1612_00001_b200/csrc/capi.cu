@@ -557,11 +557,17 @@ int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_
   const cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)n, (cuuint64_t)nslots};
   const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)a->v.slot_elems * 8};
   const cuuint32_t estr[3] = {1, 1, 1};
+#if BRI_WIDE_A
+  const cuuint32_t boxA[3] = {16, 16, 1};
+  const CUtensorMapSwizzle swA = CU_TENSOR_MAP_SWIZZLE_128B;
+#else
   const cuuint32_t boxA[3] = {8, 16, 1};
+  const CUtensorMapSwizzle swA = CU_TENSOR_MAP_SWIZZLE_64B;
+#endif
   const cuuint32_t boxB[3] = {16, 128, 1};
   const cuuint32_t boxB32[3] = {16, 32, 1};
   CUresult r1 = enc(&a->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxA, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, swA,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   CUresult r2 = enc(&a->tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -2,13 +2,18 @@
 // (gemm.cu) and the fused triangular solve (trsm.cu).
 //
 // smem stage layout for a BM x BN output tile and BK = 16:
-//   A: BM/8 boxes of 8 (m) x 16 (k) doubles, SWIZZLE_64B, 1 KB each
+//   A: BM/16 boxes of 16 (m) x 16 (k) doubles, SWIZZLE_128B, 2 KB each
+//      (BRI_WIDE_A=0: BM/8 boxes of 8 x 16, SWIZZLE_64B — twice the TMA ops)
 //   B: one box of 16 (k) x BN (n) doubles, SWIZZLE_128B
-// Both swizzles make the m16n8k4 fragment loads conflict-free (2 wavefronts
+// The swizzles make the m16n8k4 fragment loads conflict-free (2 wavefronts
 // per 32 x 8 B request, the minimum).
 #pragma once
 
 #include "bri_common.cuh"
+
+#ifndef BRI_WIDE_A
+#define BRI_WIDE_A 1
+#endif
 
 namespace bri {
 
@@ -26,8 +31,13 @@ template <int BM, int BN>
 BRI_DEVI void tile_issue(uint8_t* st, uint64_t* full, const CUtensorMap* tmA, const CUtensorMap* tmB,
                          int a_row, int a_col, int a_slot, int b_row, int b_col, int b_slot) {
   mbar_arrive_expect_tx(full, StageGeom<BM, BN>::BYTES);
+#if BRI_WIDE_A
+#pragma unroll
+  for (int ob = 0; ob < BM / 16; ++ob) tma_load_3d(st + ob * 2048, tmA, full, a_row + ob * 16, a_col, a_slot);
+#else
 #pragma unroll
   for (int ob = 0; ob < BM / 8; ++ob) tma_load_3d(st + ob * 1024, tmA, full, a_row + ob * 8, a_col, a_slot);
+#endif
   tma_load_3d(st + StageGeom<BM, BN>::A_BYTES, tmB, full, b_row, b_col, b_slot);
 }
 
@@ -48,12 +58,28 @@ struct WarpAcc {
   // Consume one k-tile: A rows [wm0, wm0 + 16*MI), B cols [wn0, wn0 + 8*NJ).
   // Lanes whose k index is >= kvalid contribute zeros (K tail).
   BRI_DEVI void mma_stage(const uint8_t* sA, const uint8_t* sB, int kvalid, int wm0, int wn0, int lane) {
+    mma_stage_steps<0, 1>(sA, sB, kvalid, wm0, wn0, lane);
+  }
+
+  // Only the k4-steps KS0, KS0 + KSTRIDE, ... of the stage (k split across warp groups).
+  template <int KS0, int KSTRIDE>
+  BRI_DEVI void mma_stage_steps(const uint8_t* sA, const uint8_t* sB, int kvalid, int wm0, int wn0, int lane) {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int kk = 0; kk < TILE_BK / 4; ++kk) {
+    for (int kk = KS0; kk < TILE_BK / 4; kk += KSTRIDE) {
       const int k = kk * 4 + t;
       const bool kin = k < kvalid;
       double a[MI][2], bf[NJ];
+#if BRI_WIDE_A
+      const uint32_t sw = (k & 7) << 4;
+      const uint32_t off0 = k * 128 + ((g * 8) ^ sw), off1 = k * 128 + (((g + 8) * 8) ^ sw);
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const uint8_t* box = sA + ((wm0 + i * 16) >> 4) * 2048;
+        a[i][0] = kin ? *reinterpret_cast<const double*>(box + off0) : 0.0;
+        a[i][1] = kin ? *reinterpret_cast<const double*>(box + off1) : 0.0;
+      }
+#else
       uint32_t offa = k * 64 + g * 8;
       offa ^= ((offa >> 7) & 3) << 4;
 #pragma unroll
@@ -62,6 +88,7 @@ struct WarpAcc {
         a[i][0] = kin ? *reinterpret_cast<const double*>(sA + ob * 1024 + offa) : 0.0;
         a[i][1] = kin ? *reinterpret_cast<const double*>(sA + (ob + 1) * 1024 + offa) : 0.0;
       }
+#endif
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
         const int n = wn0 + j * 8 + g;

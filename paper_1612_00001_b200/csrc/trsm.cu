@@ -25,13 +25,17 @@ namespace {
 
 constexpr int T = TRSM_BLOCK;      // 64
 constexpr int BN = 32;             // right-hand-side columns per CTA
-constexpr int STAGES = 3;      // 3 stages keep two CTAs resident per SM (latency hiding across solves)
+// Ring depth: a 64 x 32 k-tile is consumed in ~0.25 us, so ~1.5 us of TMA
+// latency needs ~6 tiles in flight per SM: 7 stages when the grid gives each
+// SM one CTA, 3 (two CTAs resident per SM) for large batches.
+constexpr int STAGES_DEEP = 7, STAGES_WIDE = 3;
 constexpr int THREADS = 256;
 constexpr int STAGE_BYTES = StageGeom<T, BN>::BYTES;  // 12 KB
 constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
 constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
 constexpr int LDB = T + 4;         // prefetched B_i tile stride ([n][k])
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256;
+template <int STAGES>
+constexpr int smem_bytes() { return STAGES * STAGE_BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256; }
 
 BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
@@ -106,7 +110,7 @@ struct TrsmArgs {
                         // being inverted): rows above a column's diagonal are zero and stay zero
 };
 
-template <bool LOWER>
+template <bool LOWER, int STAGES>
 __global__ void __launch_bounds__(THREADS, 2)
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
   extern __shared__ uint8_t smem_raw[];
@@ -126,8 +130,13 @@ __global__ void __launch_bounds__(THREADS, 2)
   double* W = p.base + (long long)ws * p.slot_elems;
   const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
   const int nb = (p.nr + T - 1) / T;
-  const int wm0 = (warp & 3) * 16;   // 4 warps along M (16 rows each)
-  const int wn0 = (warp >> 2) * 16;  // 2 warps along N (16 cols each)
+  // K loop: two warp groups split every stage's k4-steps (even / odd), each
+  // warp owning 16 rows x all 32 columns: four independent accumulator chains
+  // per warp keep the DMMA pipe fed; the halves are summed in smem.
+  const int kg = warp >> 2;
+  const int wm0 = (warp & 3) * 16;
+  // the Tinv * R product: 4 warps along M x 2 along N, 16 x 16 each
+  const int xm0 = (warp & 3) * 16, xn0 = (warp >> 2) * 16;
   const bool producer = (warp == 0 && lane == 0);
 
   if (threadIdx.x == 0) {
@@ -143,7 +152,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     tma_prefetch_desc(&tmB);
   }
 
-  int it = 0;  // k-tiles consumed so far (ring position / phase)
+  int it = 0;   // k-tiles consumed so far (ring position / phase)
+  int pre = 0;  // k-tiles of the current block row already issued during the previous one
   // first block row with nonzeros in this CTA's columns (triangular right-hand side)
   const int i0 = (LOWER && p.tri_rhs) ? max(0, (c0 - p.r0) / T) : 0;
   for (int ii = LOWER ? i0 : 0; ii < nb; ++ii) {
@@ -160,7 +170,8 @@ __global__ void __launch_bounds__(THREADS, 2)
                         klo + kt * TILE_BK, c0, ws);
     };
     if (producer)
-      for (int kt = 0; kt < STAGES && kt < KT; ++kt) issue(kt);
+      for (int kt = pre; kt < STAGES && kt < KT; ++kt) issue(kt);
+    pre = 0;
     // prefetch Tinv_ii and B_i with cp.async; they land while the K loop runs
     {
       const double* Di = dinv + (long long)(row0 / T) * T * T;
@@ -176,13 +187,16 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    WarpAcc<1, 2> acc;
+    WarpAcc<1, 4> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
       const int s = (it + kt) % STAGES;
       mbar_wait(&full[s], ((it + kt) / STAGES) & 1);
       const uint8_t* sA = smem + s * STAGE_BYTES;
-      acc.mma_stage(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, wn0, lane);
+      if (kg == 0)
+        acc.mma_stage_steps<0, 2>(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, 0, lane);
+      else
+        acc.mma_stage_steps<1, 2>(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, 0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (producer && kt >= 1) {
@@ -195,19 +209,47 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     // (the epilogue's __syncthreads below ends every read of the ring before reuse)
     it += KT;
+    // Lower sweep: the next block row's first k-tiles read only X rows finished
+    // before this one, so they load while this row's epilogue runs (each ring
+    // slot once its last reader released it).
+    if (LOWER && producer && ii + 1 < nb) {
+      const int row0n = row0 + T;
+      const int KTn = (row0n - klo + TILE_BK - 1) / TILE_BK;
+      const int safe = min(min(STAGES, KT), KTn);
+      for (int kt = 0; kt < safe; ++kt) {
+        const int q = it + kt;
+        if (q >= STAGES) mbar_wait(&empty[q % STAGES], ((q / STAGES) - 1) & 1);
+        tile_issue<T, BN>(smem + (q % STAGES) * STAGE_BYTES, &full[q % STAGES], &tmA, &tmB, row0n,
+                          klo + kt * TILE_BK, fs, klo + kt * TILE_BK, c0, ws);
+      }
+      pre = safe;
+    }
 
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    // R = B_i - acc  (rows >= rows and columns >= nrhs are zero)
+    // R = B_i - (acc_even + acc_odd)  (rows >= rows and columns >= nrhs are zero)
+    if (kg == 1) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int r = wm0 + g + ((v >> 1) << 3);
-        const int cc = wn0 + j * 8 + 2 * t + (v & 1);
-        const bool ok = r < rows && c0 + cc < cend;
-        R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - acc.c[0][j][v] : 0.0;
-      }
+        for (int v = 0; v < 4; ++v) {
+          const int r = wm0 + g + ((v >> 1) << 3);
+          const int cc = j * 8 + 2 * t + (v & 1);
+          R[cc * LDR + r] = acc.c[0][j][v];
+        }
+    }
+    __syncthreads();
+    if (kg == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int r = wm0 + g + ((v >> 1) << 3);
+          const int cc = j * 8 + 2 * t + (v & 1);
+          const bool ok = r < rows && c0 + cc < cend;
+          R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - (acc.c[0][j][v] + R[cc * LDR + r]) : 0.0;
+        }
+    }
     __syncthreads();
     // X_i = Tinv_ii * R   (64 x 32 x 64 DMMA from smem)
     double x[2][4];
@@ -217,11 +259,11 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int v = 0; v < 4; ++v) x[j][v] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < T; k0 += 4) {
-      const double a0 = D[(k0 + t) * LDD + wm0 + g];
-      const double a1 = D[(k0 + t) * LDD + wm0 + g + 8];
+      const double a0 = D[(k0 + t) * LDD + xm0 + g];
+      const double a1 = D[(k0 + t) * LDD + xm0 + g + 8];
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const double b0 = R[(wn0 + j * 8 + g) * LDR + k0 + t];
+        const double b0 = R[(xn0 + j * 8 + g) * LDR + k0 + t];
         dmma_16x8x4(x[j], a0, a1, b0);
       }
     }
@@ -229,8 +271,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int r = wm0 + g + ((v >> 1) << 3);
-        const int cc = wn0 + j * 8 + 2 * t + (v & 1);
+        const int r = xm0 + g + ((v >> 1) << 3);
+        const int cc = xn0 + j * 8 + 2 * t + (v & 1);
         if (r < rows && c0 + cc < cend) W[(long long)(row0 + r) + (long long)(c0 + cc) * p.ld] = x[j][v];
       }
     // the next block rows read these X rows through TMA (async proxy)
@@ -241,12 +283,17 @@ __global__ void __launch_bounds__(THREADS, 2)
 
 }  // namespace
 
-int trsm_smem_bytes() { return SMEM_BYTES; }
+int trsm_smem_bytes() { return smem_bytes<STAGES_DEEP>(); }
 
 cudaError_t configure_trsm() {
-  cudaError_t e = cudaFuncSetAttribute(trsm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(trsm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* f, int bytes) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  };
+  set((const void*)trsm_kernel<true, STAGES_DEEP>, smem_bytes<STAGES_DEEP>());
+  set((const void*)trsm_kernel<false, STAGES_DEEP>, smem_bytes<STAGES_DEEP>());
+  set((const void*)trsm_kernel<true, STAGES_WIDE>, smem_bytes<STAGES_WIDE>());
+  set((const void*)trsm_kernel<false, STAGES_WIDE>, smem_bytes<STAGES_WIDE>());
   return e;
 }
 
@@ -279,11 +326,21 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
   p.nrhs = nrhs;
   p.tri_rhs = tri_rhs ? 1 : 0;
   dim3 grid((nrhs + BN - 1) / BN, count);
+  static const int sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  const bool deep = (long long)grid.x * grid.y <= sms;
   count_launch();
-  if (lower)
-    trsm_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB32, p);
-  else
-    trsm_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB32, p);
+  if (deep) {
+    if (lower) trsm_kernel<true, STAGES_DEEP><<<grid, THREADS, smem_bytes<STAGES_DEEP>(), s>>>(tmA, tmB32, p);
+    else trsm_kernel<false, STAGES_DEEP><<<grid, THREADS, smem_bytes<STAGES_DEEP>(), s>>>(tmA, tmB32, p);
+  } else {
+    if (lower) trsm_kernel<true, STAGES_WIDE><<<grid, THREADS, smem_bytes<STAGES_WIDE>(), s>>>(tmA, tmB32, p);
+    else trsm_kernel<false, STAGES_WIDE><<<grid, THREADS, smem_bytes<STAGES_WIDE>(), s>>>(tmA, tmB32, p);
+  }
   return cudaGetLastError();
 }
 
