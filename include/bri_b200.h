@@ -147,6 +147,25 @@ int bri_rbf_blocks(bri_arena* arena, void* stream, const double* x, int n, int d
 int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, double ridge, double* out,
                   long long ldo);
 
+/*
+ * Host -> device block loads — the fetch of providers.py:318-336 for a matrix in
+ * (pinned) host memory: one 2-D async copy per item (block row i, block col j,
+ * slot), 0-based, from the row-major host matrix with leading dim ldh into the
+ * slot's row-major b x b window.  Pinned host memory keeps the copies
+ * asynchronous on `stream`.
+ */
+int bri_load_host_blocks(bri_arena* arena, void* stream, const double* host, long long ldh, int count,
+                         const int* items);
+
+/*
+ * bri_schur_batch with input gates: the stream waits on ev_l (an event, may be
+ * NULL) before reading the l operands and on ev_rtr before reading rt and r,
+ * so the pivot factorization overlaps the copies of the other operands.  The
+ * p operands must be resident when the call is issued.  Not graph-captured.
+ */
+int bri_schur_batch_gated(bri_arena* arena, void* stream, int count, const int* items, int* status, void* ev_l,
+                          void* ev_rtr);
+
 /* FP64 DMMA throughput probe (register-only mma.sync loop on every SM);
  * writes achieved TFLOP/s.  Used by bench.py as the roofline denominator. */
 int bri_fp64_peak(void* stream, int iters, double* tflops);

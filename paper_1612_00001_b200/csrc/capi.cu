@@ -741,7 +741,15 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
   return 0;
 }
 
+int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* items, int* status, void* ev_l,
+                          void* ev_rtr);
+
 int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
+  return bri_schur_batch_gated(ar, stream, count, items, status, nullptr, nullptr);
+}
+
+int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* items, int* status, void* ev_l,
+                          void* ev_rtr) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_schur_batch: bad arguments");
   if (count == 0) return 0;
   if (ar->v.n > max_panel_rows())
@@ -756,6 +764,8 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
       for (int k = 0; k < 5; ++k) h[5 * i + k] = I(i, k);
     int* dev = nullptr;
     if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+    if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), 0));
+    if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), 0));
     BRI_CHECK(launch_small_node(ar->v, dev, count, 0, status, s));
     return 0;
   }
@@ -795,11 +805,19 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
   BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
   if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc)) return rc;
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
+  if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), 0));
   BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
   if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count)) return rc;
+  if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), 0));
   return gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
   };
-  if (int rc = run_graphed(ar->ctx, s, graph_key(0, ar, count, dev), issue)) return rc;
+  // gated runs wait on input copies still in flight: issued directly (a graph
+  // would freeze the events), everything else replays a captured graph
+  if (ev_l || ev_rtr) {
+    if (int rc = issue(s)) return rc;
+  } else if (int rc = run_graphed(ar->ctx, s, graph_key(0, ar, count, dev), issue)) {
+    return rc;
+  }
   if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
   return 0;
 }
@@ -832,6 +850,23 @@ int bri_gather_elements(bri_arena* ar, void* stream, const double* M, long long 
   bri::count_launch();
   gather_elements_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, m, rmap, cmap, dev);
   BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_load_host_blocks(bri_arena* ar, void* stream, const double* host, long long ldh, int count,
+                         const int* items) {
+  if (ar == nullptr || host == nullptr || items == nullptr || count < 0 || ldh < ar->v.n)
+    return fail_msg("bri_load_host_blocks: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  for (int q = 0; q < count; ++q) {
+    const int i = items[3 * q], j = items[3 * q + 1], slot = items[3 * q + 2];
+    if (i < 0 || j < 0 || slot < 0 || slot >= ar->v.nslots) return fail_msg("bri_load_host_blocks: bad item");
+    const double* src = host + (long long)i * n * ldh + (long long)j * n;
+    double* dst = ar->v.base + (long long)slot * ar->v.slot_elems;
+    BRI_CHECK(cudaMemcpy2DAsync(dst, (size_t)ar->v.ld * 8, src, (size_t)ldh * 8, (size_t)n * 8, (size_t)n,
+                                cudaMemcpyHostToDevice, s));
+  }
   return 0;
 }
 

@@ -36,6 +36,24 @@ def stream_handle(device: int):
     return ctypes.c_void_p(_torch().cuda.current_stream(device).cuda_stream)
 
 
+_FREE0: dict = {}
+
+
+def free_bytes(device: int) -> int:
+    """Device memory available to this process: free + PyTorch's cached-but-unused.
+
+    cudaMemGetInfo costs milliseconds (occasionally ~100 ms) per call, so it is
+    queried once per device; afterwards the estimate follows PyTorch's own
+    reservations (other processes' later allocations are not seen)."""
+    torch = _torch()
+    if device not in _FREE0:
+        free, _ = torch.cuda.mem_get_info(device)
+        _FREE0[device] = (free, torch.cuda.memory_reserved(device))
+    free0, res0 = _FREE0[device]
+    reserved = torch.cuda.memory_reserved(device)
+    return max(0, free0 - (reserved - res0)) + (reserved - torch.cuda.memory_allocated(device))
+
+
 def padded_ld(n: int) -> int:
     return (n + 7) // 8 * 8
 
@@ -114,6 +132,22 @@ class Arena:
         flat = [s for it in items for s in it]
         _native.check(self.lib.bri_schur_batch(self.handle, self.stream, len(items), self._items(flat),
                                                ctypes.c_void_p(status.data_ptr())), "bri_schur_batch")
+
+    def schur_gated(self, items, status, ev_l, ev_rtr) -> None:
+        """schur() whose l / (rt, r) operands may still be in flight: the stream waits on
+        the torch.cuda.Events ev_l / ev_rtr (or None) before reading them."""
+        flat = [s for it in items for s in it]
+        h = lambda ev: ctypes.c_void_p(ev.cuda_event) if ev is not None else None
+        _native.check(self.lib.bri_schur_batch_gated(self.handle, self.stream, len(items), self._items(flat),
+                                                     ctypes.c_void_p(status.data_ptr()), h(ev_l), h(ev_rtr)),
+                      "bri_schur_batch_gated")
+
+    def load_host(self, host, items, stream=None) -> None:
+        """Copy blocks of a pinned row-major host tensor into slots: items (block row, block col, slot), 0-based."""
+        flat = [s for it in items for s in it]
+        st = self.stream if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        _native.check(self.lib.bri_load_host_blocks(self.handle, st, ctypes.c_void_p(host.data_ptr()), host.stride(0),
+                                                    len(items), self._items(flat)), "bri_load_host_blocks")
 
     def invert(self, items, status) -> None:
         """items: list of (in, f, out)."""

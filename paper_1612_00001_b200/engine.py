@@ -37,7 +37,7 @@ import numpy as np
 
 from .core import Block, Workspace
 from .dag import build_from_specs, build_schedule, target_maps
-from .device import Arena, cached_arena, cached_bytes, current_device, padded_ld
+from .device import Arena, cached_arena, cached_bytes, current_device, free_bytes, padded_ld
 from .errors import (BadPartitionError, DimensionMismatchError, IndexOutOfRangeError,
                      SingularBlockError, SingularPivotError)
 from .frames import PLAN, Frame, Quadrant, root_frame, split_frame
@@ -113,6 +113,41 @@ class _HostSource:
                     pending[n + R] = pool.submit(self._read, idx, items[n + R][:2])
 
 
+_COPY_STREAMS: dict = {}
+
+
+class _PinnedSource:
+    """Matrix in pinned host memory, not resident on the device: the blocks a
+    run needs are copied host -> slot (2-D async copies) on a dedicated copy
+    stream, in the order the run first reads them.  `load` makes the caller's
+    stream wait for its copies; `load_gated` instead returns events so a DAG
+    level can factor its pivots while the other operands are still in flight."""
+
+    def __init__(self, pinned, b: int, device: int):
+        torch = _torch()
+        self.t, self.b, self.device = pinned, b, device
+        if device not in _COPY_STREAMS:
+            _COPY_STREAMS[device] = torch.cuda.Stream(device)
+        self.copy = _COPY_STREAMS[device]
+
+    def _issue(self, arena: Arena, items):
+        torch = _torch()
+        self.copy.wait_stream(torch.cuda.current_stream(self.device))   # slots may have been in use
+        arena.load_host(self.t, [(i - 1, j - 1, s) for i, j, s in items], stream=self.copy)
+        ev = torch.cuda.Event()
+        ev.record(self.copy)
+        return ev
+
+    def load(self, arena: Arena, items) -> None:
+        items = list(items)
+        if items:
+            _torch().cuda.current_stream(self.device).wait_event(self._issue(arena, items))
+
+    def load_gated(self, arena: Arena, groups):
+        """groups: item lists in first-use order; returns one event per group."""
+        return [self._issue(arena, g) if g else None for g in groups]
+
+
 class _WindowSource:
     """Padded layouts: view blocks gathered element-wise from M on the device."""
 
@@ -147,6 +182,8 @@ def _source_for(provider: BlockProvider, device: int):
     lay = base.layout
     if hasattr(base, "_generator"):
         return _GenSource(base._generator(), lay.b, None, None, device), base, mr, mc
+    if lay.l == 0 and getattr(base, "_pinned", None) is not None and device not in base._dev:
+        return _PinnedSource(base._pinned, lay.b, device), base, mr, mc
     dm = base._device_matrix(device)
     if lay.l != 0:
         if dm is None:
@@ -185,9 +222,7 @@ def _budget_slots(ws: Workspace, b: int, device: int) -> int:
     if ws.arena_bytes is not None:
         budget = ws.arena_bytes
     else:
-        free, _ = torch.cuda.mem_get_info(device)
-        cached = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
-        budget = int((free + cached + cached_bytes(device, b)) * 0.85)
+        budget = int((free_bytes(device) + cached_bytes(device, b)) * 0.85)
     return max(1, budget // block_bytes)
 
 
@@ -218,7 +253,30 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
         mslot = {}
         for ij in used:
             mslot[ij] = arena.alloc()
-        src.load(arena, [(i, j, s) for (i, j), s in mslot.items()])
+        gates = None
+        if isinstance(src, _PinnedSource) and len(levels[min(levels)]) <= chunk:
+            # copy in first-use order: the level's pivots, then l, then rt and r;
+            # the pivots' factorization starts as soon as they have landed
+            first = [sched.nodes[nid] for nid in levels[min(levels)]]
+            order, seen = [], set()
+            for roles in ((0,), (2,), (1, 3)):
+                grp = []
+                for node in first:
+                    for q in roles:
+                        r = node.operands[q]
+                        if r[0] == "m" and (r[1], r[2]) not in seen:
+                            seen.add((r[1], r[2]))
+                            grp.append((r[1], r[2], mslot[(r[1], r[2])]))
+                order.append(grp)
+            rest = [(i, j, s) for (i, j), s in mslot.items() if (i, j) not in seen]
+            ev_p, ev_l, ev_rtr = src.load_gated(arena, order)
+            if rest:
+                src.load(arena, rest)
+            if ev_p is not None:
+                torch.cuda.current_stream(device).wait_event(ev_p)
+            gates = (ev_l, ev_rtr)
+        else:
+            src.load(arena, [(i, j, s) for (i, j), s in mslot.items()])
         val = {}
         pos = {}
         prev = None
@@ -235,7 +293,11 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                     pos[nid] = len(pos)
                     scratch += (f, w)
                 base = pos[part[0]]
-                arena.schur(items, status[base:base + len(part)])
+                if gates is not None:
+                    arena.schur_gated(items, status[base:base + len(part)], *gates)
+                    gates = None
+                else:
+                    arena.schur(items, status[base:base + len(part)])
                 for s in scratch:
                     arena.release(s)
             if not keep_all:

@@ -278,10 +278,10 @@ class _MemoryProvider(_MatrixElements, BlockProvider):
         if t is None:
             import torch
 
+            from .device import free_bytes
+
             m = self.layout.m
-            free, _ = torch.cuda.mem_get_info(device)
-            spare = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
-            if 8 * m * m > RESIDENT_FRACTION * (free + spare):
+            if 8 * m * m > RESIDENT_FRACTION * free_bytes(device):
                 return None
             if self._pinned is not None:  # pinned host tensor: one async H2D copy
                 t = self._pinned.to(f"cuda:{device}", non_blocking=True)
