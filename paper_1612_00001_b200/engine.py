@@ -31,6 +31,7 @@ reduction raises SingularBlockError (core.py:252-254).
 from __future__ import annotations
 
 import time
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -427,11 +428,30 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
     return results, info
 
 
-def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots):
+_SCHED_CACHE: "OrderedDict" = OrderedDict()
+
+
+def _schedule(key, k, specs, paths0):
+    """build_from_specs, memoized for plain target lists (key not None): a
+    schedule is immutable once built and depends only on (k, targets)."""
+    if key is None:
+        return build_from_specs(k, specs, paths0)
+    sched = _SCHED_CACHE.get(key)
+    if sched is None:
+        sched = build_from_specs(k, specs, paths0)
+        _SCHED_CACHE[key] = sched
+        if len(_SCHED_CACHE) > 64:
+            _SCHED_CACHE.popitem(last=False)
+    else:
+        _SCHED_CACHE.move_to_end(key)
+    return sched
+
+
+def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots, key=None):
     """DAG run over all roots; if the union does not fit the arena, split the
     roots into halves (shared nodes are recomputed, memory stays bounded).
     Groups run in root order, so the first error raised is the reference's."""
-    sched = build_from_specs(k, specs, paths0)
+    sched = _schedule(key, k, specs, paths0)
     try:
         tensors, info = _run_dag(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
         return tensors, info, [sched]
@@ -441,8 +461,10 @@ def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots):
     h = len(specs) // 2
     p0 = paths0[:h] if paths0 is not None else None
     p1 = paths0[h:] if paths0 is not None else None
-    t0, i0, s0 = _run_grouped(src, k, specs[:h], p0, ws, device, trace, invert_roots)
-    t1, i1, s1 = _run_grouped(src, k, specs[h:], p1, ws, device, trace, invert_roots)
+    k0 = None if key is None else key + ("lo", h)
+    k1 = None if key is None else key + ("hi", h)
+    t0, i0, s0 = _run_grouped(src, k, specs[:h], p0, ws, device, trace, invert_roots, k0)
+    t1, i1, s1 = _run_grouped(src, k, specs[h:], p1, ws, device, trace, invert_roots, k1)
     i0.dag_nodes += i1.dag_nodes
     i0.tree_nodes += i1.tree_nodes
     i0.targets += i1.targets
@@ -490,16 +512,17 @@ def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, inver
     src, base, mr, mc = _source_for(provider, device)
     k = base.layout.k
     specs = specs_fn(mr, mc)
+    key = (k, tuple(targets)) if (targets is not None and mr is None and mc is None and paths0 is None) else None
     if ws.schedule == "tree":
-        sched = build_from_specs(k, specs, paths0)
+        sched = _schedule(key, k, specs, paths0)
         tensors, info = _run_tree(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
         scheds = [sched]
     else:
-        tensors, info, scheds = _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots)
+        tensors, info, scheds = _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots, key)
     executed_nodes = sum(len(s.nodes) for s in scheds)
     sched = scheds[0]
     if len(scheds) > 1:
-        sched = build_from_specs(k, specs, paths0)
+        sched = _schedule(key, k, specs, paths0)
     # reference accounting (tree semantics), per root
     for t in range(len(sched.specs)):
         ws.counters.add_nodes(sched.tree_nodes(t), targets=1 if invert_roots else 0)
