@@ -27,7 +27,8 @@ cudaError_t configure_trsm();
 constexpr int NBMAX = 32;        // LU panel width upper bound
 constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
 constexpr int TRSM_BLOCK = 64;   // diagonal block of the fused triangular solve
-constexpr int TRSM_LEAF = 512;   // recursive solves hand sub-triangles up to this size to trsm.cu
+constexpr int TRSM_LEAF = 512;
+constexpr int LU_OUTER = 128;   // outer block width of the two-level LU (multiple of TRSM_BLOCK and NBMAX)   // recursive solves hand sub-triangles up to this size to trsm.cu
 
 // Arena geometry: nslots column-major n x n blocks (X-world), leading dim ld
 // (multiple of 8, >= n), slot i at base + i * slot_elems.

@@ -201,7 +201,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   BRI_CHECK(launch_pi_init(sc.pi, n, count, s));
   BRI_CHECK(launch_maxabs(v, dev_slots, count, sc.scale_bits, s));
   const int nbi = panel_width(n);
-  const int outer = 128;  // multiple of TRSM_BLOCK and of every inner width
+  const int outer = LU_OUTER;
   const size_t per = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
   if (int rc = ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
   double* dl = static_cast<double*>(ctx->dinv.ptr);
@@ -289,14 +289,18 @@ int ensure_dinv(bri_arena* ar, cudaStream_t s, int count) {
 }
 
 // Inverted 64 x 64 diagonal blocks of L and U for `count` factors (ctx->dinv):
-// returns pointers to the L and U tables.
-int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, double** dl, double** du) {
+// returns pointers to the L and U tables.  after_getrf: the factorization was
+// just computed by getrf_device on this stream, which already inverted every
+// L diagonal block but those of its last outer block.
+int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, double** dl, double** du,
+              bool after_getrf = false) {
   const int n = ar->v.n;
   const size_t per = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
   if (int rc = ar->ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
   *dl = static_cast<double*>(ar->ctx->dinv.ptr);
   *du = *dl + per * count;
-  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, 0, 0, s));
+  const int l0 = after_getrf ? ((n - 1) / LU_OUTER) * LU_OUTER / TRSM_BLOCK : 0;
+  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, l0, 0, s));
   BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, false, *du, 0, 0, s));
   return 0;
 }
@@ -334,9 +338,9 @@ int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, i
 
 // Both sweeps of dgetrs on W (already row-permuted): L then U.
 int getrs_sweeps(bri_arena* ar, cudaStream_t s, const int* dev_f, const int* fw, const int* gemm_fw, int count,
-                 bool tri_rhs = false) {
+                 bool tri_rhs = false, bool after_getrf = false) {
   double *dl = nullptr, *du = nullptr;
-  if (int rc = make_dinv(ar, s, dev_f, count, &dl, &du)) return rc;
+  if (int rc = make_dinv(ar, s, dev_f, count, &dl, &du, after_getrf)) return rc;
   const int n = ar->v.n;
   if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, 0, n, n, dl, tri_rhs)) return rc;
   return trsm_rec(ar, s, fw, gemm_fw, count, false, 0, n, n, du);
@@ -731,7 +735,7 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
     // column permutation X^-1[:, pi[x]] = T[:, x].  T lives in `out`, the
     // permuted result goes to f (the factors are no longer needed) and back.
     BRI_CHECK(launch_identity(ar->v, d_fo + 1, 2, count, st));
-    if (int rc = getrs_sweeps(ar, st, d_f, d_fo, d_fooo, count, true)) return rc;
+    if (int rc = getrs_sweeps(ar, st, d_f, d_fo, d_fooo, count, true, true)) return rc;
     BRI_CHECK(launch_colscatter(ar->v, d_of, count, sc.pi, n, st));
     BRI_CHECK(launch_copy(ar->v, d_fo, count, st));
     return 0;
@@ -807,7 +811,7 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
   if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), 0));
   BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
-  if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count)) return rc;
+  if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count, false, true)) return rc;
   if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), 0));
   return gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
   };
