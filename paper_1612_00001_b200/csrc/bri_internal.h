@@ -97,9 +97,9 @@ cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
 int trsm_smem_bytes();
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
                         int blk0, int nblocks, cudaStream_t s);
-cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
-                              const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int c_off, int nrhs, bool tri_rhs, cudaStream_t s);
+cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const CUtensorMap& tmB16,
+                              const ArenaView& a, const int* fw, int count, const double* dinv, bool lower, int r0,
+                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s);
 
 // Fused one-CTA node / inverse for n <= SMALL_MAX.
 // items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.

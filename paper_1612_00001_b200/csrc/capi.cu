@@ -102,6 +102,7 @@ struct bri_arena {
   alignas(64) CUtensorMap tmA;
   alignas(64) CUtensorMap tmB;
   alignas(64) CUtensorMap tmB32;
+  alignas(64) CUtensorMap tmB16;
 };
 
 namespace {
@@ -226,7 +227,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   // the critical path that factors the next block concurrently)
   auto update_cols = [&](cudaStream_t st, int J0, int W, int pidx0, int c0, int c1, int cap) -> int {
     if (c1 <= c0) return 0;
-    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, v, dev_ff, count, dl, true, J0, W, c0, c1 - c0, false, st));
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, v, dev_ff, count, dl, true, J0, W, c0, c1 - c0, false, st));
     return gemm_call(ar, st, dev_ffff, count, n - J0 - W, c1 - c0, W, J0 + W, J0, J0, c0, J0 + W, c0, -1.0, 1.0,
                      cap);
   };
@@ -316,7 +317,7 @@ int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, i
              int r0, int nr, int nrhs, const double* dinv, bool tri = false) {
   const int ncol = tri ? (r0 + nr < nrhs ? r0 + nr : nrhs) : nrhs;
   if (nr <= TRSM_LEAF) {
-    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->v, fw, count, dinv, lower, r0, nr, 0, ncol, tri, s));
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, ar->v, fw, count, dinv, lower, r0, nr, 0, ncol, tri, s));
     return 0;
   }
   int h = ((nr / 2) + TRSM_BLOCK - 1) / TRSM_BLOCK * TRSM_BLOCK;
@@ -570,6 +571,7 @@ int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_
 #endif
   const cuuint32_t boxB[3] = {16, 128, 1};
   const cuuint32_t boxB32[3] = {16, 32, 1};
+  const cuuint32_t boxB16[3] = {16, 16, 1};
   CUresult r1 = enc(&a->tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxA, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, swA,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -579,7 +581,10 @@ int bri_arena_create(bri_ctx* ctx, double* base, int n, int ld, int nslots, bri_
   CUresult r3 = enc(&a->tmB32, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB32, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) {
+  CUresult r4 = enc(&a->tmB16, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxB16, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS || r4 != CUDA_SUCCESS) {
     delete a;
     return fail_msg("cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" + std::to_string((int)r2));
   }

@@ -24,18 +24,18 @@ namespace bri {
 namespace {
 
 constexpr int T = TRSM_BLOCK;      // 64
-constexpr int BN = 32;             // right-hand-side columns per CTA
-// Ring depth: a 64 x 32 k-tile is consumed in ~0.25 us, so ~1.5 us of TMA
-// latency needs ~6 tiles in flight per SM: 7 stages when the grid gives each
-// SM one CTA, 3 (two CTAs resident per SM) for large batches.
-constexpr int STAGES_DEEP = 7, STAGES_WIDE = 3;
+// Variants (right-hand-side columns per CTA, ring depth):
+//   <32, 3>: large batches, two CTAs per SM;
+//   <16, 4>: a grid of <= one CTA per SM at 32 columns (a single factor's solve)
+//            is split twice as fine, again two CTAs per SM to hide the per-block-row latency.
 constexpr int THREADS = 256;
-constexpr int STAGE_BYTES = StageGeom<T, BN>::BYTES;  // 12 KB
 constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
 constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
 constexpr int LDB = T + 4;         // prefetched B_i tile stride ([n][k])
-template <int STAGES>
-constexpr int smem_bytes() { return STAGES * STAGE_BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256; }
+template <int BN, int STAGES>
+constexpr int smem_bytes() {
+  return STAGES * StageGeom<T, BN>::BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256;
+}
 
 BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem_dst)), "l"(gsrc),
@@ -110,12 +110,15 @@ struct TrsmArgs {
                         // being inverted): rows above a column's diagonal are zero and stay zero
 };
 
-template <bool LOWER, int STAGES>
+template <bool LOWER, int BN, int STAGES>
 __global__ void __launch_bounds__(THREADS, 2)
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
+  constexpr int SB = StageGeom<T, BN>::BYTES;
+  constexpr int NJ = BN / 8;        // n8 tiles per warp in the K loop (16 x BN per warp)
+  constexpr int XJ = BN / 16;       // n8 tiles per warp in the Tinv * R product
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  double* D = reinterpret_cast<double*>(smem + STAGES * STAGE_BYTES);   // Tinv_ii, [k][m] col-major (LDD)
+  double* D = reinterpret_cast<double*>(smem + STAGES * SB);   // Tinv_ii, [k][m] col-major (LDD)
   double* R = D + T * LDD;                                              // B_i - acc, [n][k] (LDR)
   double* Bst = R + BN * LDR;                                           // prefetched B_i, [n][k] (LDB)
   uint64_t* full = reinterpret_cast<uint64_t*>(Bst + BN * LDB);
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int kg = warp >> 2;
   const int wm0 = (warp & 3) * 16;
   // the Tinv * R product: 4 warps along M x 2 along N, 16 x 16 each
-  const int xm0 = (warp & 3) * 16, xn0 = (warp >> 2) * 16;
+  const int xm0 = (warp & 3) * 16, xn0 = (warp >> 2) * (BN / 2);
   const bool producer = (warp == 0 && lane == 0);
 
   if (threadIdx.x == 0) {
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int KT = K > 0 ? (K + TILE_BK - 1) / TILE_BK : 0;
     auto issue = [&](int kt) {
       const int s = (it + kt) % STAGES;
-      tile_issue<T, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, row0, klo + kt * TILE_BK, fs,
+      tile_issue<T, BN>(smem + s * SB, &full[s], &tmA, &tmB, row0, klo + kt * TILE_BK, fs,
                         klo + kt * TILE_BK, c0, ws);
     };
     if (producer)
@@ -187,12 +190,12 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    WarpAcc<1, 4> acc;
+    WarpAcc<1, NJ> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
       const int s = (it + kt) % STAGES;
       mbar_wait(&full[s], ((it + kt) / STAGES) & 1);
-      const uint8_t* sA = smem + s * STAGE_BYTES;
+      const uint8_t* sA = smem + s * SB;
       if (kg == 0)
         acc.mma_stage_steps<0, 2>(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, 0, lane);
       else
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int kt = 0; kt < safe; ++kt) {
         const int q = it + kt;
         if (q >= STAGES) mbar_wait(&empty[q % STAGES], ((q / STAGES) - 1) & 1);
-        tile_issue<T, BN>(smem + (q % STAGES) * STAGE_BYTES, &full[q % STAGES], &tmA, &tmB, row0n,
+        tile_issue<T, BN>(smem + (q % STAGES) * SB, &full[q % STAGES], &tmA, &tmB, row0n,
                           klo + kt * TILE_BK, fs, klo + kt * TILE_BK, c0, ws);
       }
       pre = safe;
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     // R = B_i - (acc_even + acc_odd)  (rows >= rows and columns >= nrhs are zero)
     if (kg == 1) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int r = wm0 + g + ((v >> 1) << 3);
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     __syncthreads();
     if (kg == 0) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int r = wm0 + g + ((v >> 1) << 3);
@@ -251,10 +254,10 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
     }
     __syncthreads();
-    // X_i = Tinv_ii * R   (64 x 32 x 64 DMMA from smem)
-    double x[2][4];
+    // X_i = Tinv_ii * R   (64 x BN x 64 DMMA from smem)
+    double x[XJ][4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < XJ; ++j)
 #pragma unroll
       for (int v = 0; v < 4; ++v) x[j][v] = 0.0;
 #pragma unroll 4
@@ -262,13 +265,13 @@ __global__ void __launch_bounds__(THREADS, 2)
       const double a0 = D[(k0 + t) * LDD + xm0 + g];
       const double a1 = D[(k0 + t) * LDD + xm0 + g + 8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+      for (int j = 0; j < XJ; ++j) {
         const double b0 = R[(xn0 + j * 8 + g) * LDR + k0 + t];
         dmma_16x8x4(x[j], a0, a1, b0);
       }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < XJ; ++j)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const int r = xm0 + g + ((v >> 1) << 3);
@@ -283,17 +286,17 @@ __global__ void __launch_bounds__(THREADS, 2)
 
 }  // namespace
 
-int trsm_smem_bytes() { return smem_bytes<STAGES_DEEP>(); }
+int trsm_smem_bytes() { return smem_bytes<32, 3>(); }
 
 cudaError_t configure_trsm() {
   cudaError_t e = cudaSuccess;
   auto set = [&](const void* f, int bytes) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   };
-  set((const void*)trsm_kernel<true, STAGES_DEEP>, smem_bytes<STAGES_DEEP>());
-  set((const void*)trsm_kernel<false, STAGES_DEEP>, smem_bytes<STAGES_DEEP>());
-  set((const void*)trsm_kernel<true, STAGES_WIDE>, smem_bytes<STAGES_WIDE>());
-  set((const void*)trsm_kernel<false, STAGES_WIDE>, smem_bytes<STAGES_WIDE>());
+  set((const void*)trsm_kernel<true, 32, 3>, smem_bytes<32, 3>());
+  set((const void*)trsm_kernel<false, 32, 3>, smem_bytes<32, 3>());
+  set((const void*)trsm_kernel<true, 16, 4>, smem_bytes<16, 4>());
+  set((const void*)trsm_kernel<false, 16, 4>, smem_bytes<16, 4>());
   return e;
 }
 
@@ -310,9 +313,9 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
   return cudaGetLastError();
 }
 
-cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const ArenaView& a,
-                              const int* fw, int count, const double* dinv, bool lower, int r0, int nr,
-                              int c_off, int nrhs, bool tri_rhs, cudaStream_t s) {
+cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const CUtensorMap& tmB16,
+                              const ArenaView& a, const int* fw, int count, const double* dinv, bool lower, int r0,
+                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s) {
   TrsmArgs p;
   p.base = a.base;
   p.ld = a.ld;
@@ -325,21 +328,22 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
   p.c_off = c_off;
   p.nrhs = nrhs;
   p.tri_rhs = tri_rhs ? 1 : 0;
-  dim3 grid((nrhs + BN - 1) / BN, count);
   static const int sms = [] {
     int dev = 0, v = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const bool deep = (long long)grid.x * grid.y <= sms;
+  const bool fine = (long long)((nrhs + 31) / 32) * count <= sms;
   count_launch();
-  if (deep) {
-    if (lower) trsm_kernel<true, STAGES_DEEP><<<grid, THREADS, smem_bytes<STAGES_DEEP>(), s>>>(tmA, tmB32, p);
-    else trsm_kernel<false, STAGES_DEEP><<<grid, THREADS, smem_bytes<STAGES_DEEP>(), s>>>(tmA, tmB32, p);
+  if (fine) {
+    dim3 grid((nrhs + 15) / 16, count);
+    if (lower) trsm_kernel<true, 16, 4><<<grid, THREADS, smem_bytes<16, 4>(), s>>>(tmA, tmB16, p);
+    else trsm_kernel<false, 16, 4><<<grid, THREADS, smem_bytes<16, 4>(), s>>>(tmA, tmB16, p);
   } else {
-    if (lower) trsm_kernel<true, STAGES_WIDE><<<grid, THREADS, smem_bytes<STAGES_WIDE>(), s>>>(tmA, tmB32, p);
-    else trsm_kernel<false, STAGES_WIDE><<<grid, THREADS, smem_bytes<STAGES_WIDE>(), s>>>(tmA, tmB32, p);
+    dim3 grid((nrhs + 31) / 32, count);
+    if (lower) trsm_kernel<true, 32, 3><<<grid, THREADS, smem_bytes<32, 3>(), s>>>(tmA, tmB32, p);
+    else trsm_kernel<false, 32, 3><<<grid, THREADS, smem_bytes<32, 3>(), s>>>(tmA, tmB32, p);
   }
   return cudaGetLastError();
 }
