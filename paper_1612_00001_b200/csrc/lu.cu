@@ -335,17 +335,32 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     const bool swap = (pr != j && piv != 0.0);  // dgetf2 interchanges only for a nonzero pivot
     const bool recip = fabs(piv) >= kSfmin;
     const double rinv = 1.0 / piv;
+    // the finished pivot row: when it is the winning candidate its live values
+    // are in the message, and its warp stores the U row with one lane per
+    // column; otherwise (zero column pivoted in place) its owner stores it
+    int fast_slot = -1;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       if (!valid[q]) continue;
-      bool fin = false;
       if (pos[q] == j) {
-        if (swap) pos[q] = pr; else fin = true;
+        if (swap) {
+          pos[q] = pr;
+        } else if (pr == j && !none) {
+          fast_slot = q * PT + tid;
+        } else {
+          store_u_row(psm, rhp, jj, nb, q * PT + tid, x[q]);
+        }
       } else if (swap && pos[q] == pr) {
         pos[q] = j;
-        fin = true;
+        fast_slot = q * PT + tid;
       }
-      if (fin) store_u_row(psm, rhp, jj, nb, q * PT + tid, x[q]);
+    }
+    {
+      const unsigned fm = __ballot_sync(0xffffffffu, fast_slot >= 0);
+      if (fm) {
+        const int slot = __shfl_sync(0xffffffffu, fast_slot, __ffs(fm) - 1);
+        if (lane < nb - jj) psm[(jj + lane) * rhp + slot] = lds_f64(aS + 8 * (lane + 1));
+      }
     }
     PPROF(4);
     double u[PNB];
