@@ -113,14 +113,6 @@ BRI_DEVI uint32_t dsmem_addr(const void* local, uint32_t rank) {
   return out;
 }
 
-BRI_DEVI void dsmem_st_f64(uint32_t addr, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
-}
-
-BRI_DEVI void dsmem_st_s32(uint32_t addr, int v) {
-  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-
 // (value, index) argmax with LAPACK idamax tie-breaking (first index wins);
 // NaN never beats a number (|x| > best is false for NaN).
 BRI_DEVI void argmax_merge(double& v, int& i, double ov, int oi) {
@@ -153,26 +145,6 @@ BRI_DEVI void warp_argmax_fast(double& v, int& i) {
   const int mi = (int)__reduce_min_sync(0xffffffffu, best ? (unsigned)i : 0x7fffffffu);
   i = mi;
   v = (mi == 0x7fffffff) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-}
-
-// st.async: remote (cluster) shared store that signals `bytes` on the
-// destination CTA's mbarrier (complete_tx); both addresses are shared::cluster.
-BRI_DEVI void st_async_f64(uint32_t addr, double v, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
-               "l"(__double_as_longlong(v)), "r"(mbar)
-               : "memory");
-}
-
-BRI_DEVI void st_async_v2_f64(uint32_t addr, double a, double b, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(addr),
-               "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(mbar)
-               : "memory");
-}
-
-BRI_DEVI void st_async_s32(uint32_t addr, int v, uint32_t mbar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
-               "r"(mbar)
-               : "memory");
 }
 
 // Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory into a

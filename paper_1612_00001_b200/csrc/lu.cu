@@ -147,9 +147,6 @@ __device__ unsigned long long g_panel_phase[10];
 #else
 #define PPROF(k) do { } while (0)
 #endif
-#ifndef BRI_PANEL_BULK
-#define BRI_PANEL_BULK 0
-#endif
 constexpr int PT = 256;
 constexpr int PW = PT / 32;
 constexpr int PNB = NBMAX;      // live register width (narrower panels are zero-padded)
@@ -289,24 +286,10 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     if (cs > 1) {
       const bool pub = __any_sync(0xffffffffu, mine) || (cp == INT_MAX && warp == 0);
       if (pub) {
-#if BRI_PANEL_BULK
         fence_proxy_async_smem();   // generic smem writes -> visible to the bulk-copy engine
         __syncwarp();
         if (lane < cs)
           bulk_s2cluster(dsmem_addr(&cmsg[par][rank], lane), out, sizeof(CandMsg), dsmem_addr(&xbar[par], lane));
-#else
-        // 18 16-byte chunks per destination, (chunk, destination) pairs spread
-        // over the warp's lanes; each st.async completes on the peer's mbarrier
-        __syncwarp();
-        constexpr int CH = (int)(sizeof(CandMsg) / 16);
-        const uint32_t src = smem_u32(out);
-        for (int k = lane; k < CH * cs; k += 32) {
-          const int e = k % CH, d = k / CH;
-          double c0, c1;
-          lds_f64x2(src + 16 * e, c0, c1);
-          st_async_v2_f64(dsmem_addr(&cmsg[par][rank], d) + 16 * e, c0, c1, dsmem_addr(&xbar[par], d));
-        }
-#endif
       }
       PPROF(1);
       mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);
