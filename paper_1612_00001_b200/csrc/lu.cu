@@ -634,6 +634,7 @@ cudaError_t configure_lu() {
   cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
@@ -646,6 +647,9 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   // 1 row per thread while it fits a cluster of 8, else 2 (registers: 2 x 32 doubles)
   // Up to 8 x PT rows: 1 row per thread, portable clusters (measured: beats a
   // halved cluster at 2 rows); up to 8 x 2 x PT: 2 rows; beyond, 16-CTA clusters.
+  // (one row per thread on a 16-CTA cluster is faster alone at 4096 rows — 1.70
+  // vs 1.87 us/column — but a 16-SM cluster waits for SMs next to the
+  // concurrent trailing update: config 2 went from 35.0 to 39.4 ms)
   const int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
   int cs = 1;
   while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
