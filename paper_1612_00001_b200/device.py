@@ -14,6 +14,7 @@ libbri_b200.so (`_native.py`).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 from . import _native
 from .errors import BadPartitionError, DeviceError
@@ -235,24 +236,32 @@ class Arena:
 _CACHE: dict = {}
 
 
+def _cache_key(device: int):
+    # one arena per (device, thread): concurrent runs from several threads (the
+    # reference's invert_full(jobs > 1) pattern) never share slots; each thread
+    # also drives its own bri_ctx (_native.context)
+    return (device, threading.get_ident())
+
+
 def cached_arena(n: int, nslots: int, device: int, gauge=None) -> Arena:
-    """One reusable arena per device: repeated runs of the same geometry keep the
-    same device addresses (so their CUDA graphs replay) and skip reallocation."""
-    ar = _CACHE.get(device)
+    """One reusable arena per device and thread: repeated runs of the same geometry
+    keep the same device addresses (so their CUDA graphs replay) and skip reallocation."""
+    key = _cache_key(device)
+    ar = _CACHE.get(key)
     if ar is not None and ar.handle is not None and ar.n == n and ar.nslots >= nslots:
         ar.reset(gauge)
         return ar
     if ar is not None:
         ar.close()
-        _CACHE.pop(device, None)
+        _CACHE.pop(key, None)
     ar = Arena(n, nslots, device=device, gauge=gauge)
-    _CACHE[device] = ar
+    _CACHE[key] = ar
     return ar
 
 
 def cached_bytes(device: int, n: int) -> int:
-    """Device bytes held by the cached arena that a run of order n could reuse."""
-    ar = _CACHE.get(device)
+    """Device bytes held by this thread's cached arena that a run of order n could reuse."""
+    ar = _CACHE.get(_cache_key(device))
     if ar is None or ar.handle is None:
         return 0
     return ar.nslots * ar.n * ar.ld * 8

@@ -30,6 +30,7 @@ reduction raises SingularBlockError (core.py:252-254).
 
 from __future__ import annotations
 
+import threading
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -127,9 +128,10 @@ class _PinnedSource:
     def __init__(self, pinned, b: int, device: int):
         torch = _torch()
         self.t, self.b, self.device = pinned, b, device
-        if device not in _COPY_STREAMS:
-            _COPY_STREAMS[device] = torch.cuda.Stream(device)
-        self.copy = _COPY_STREAMS[device]
+        key = (device, threading.get_ident())
+        if key not in _COPY_STREAMS:
+            _COPY_STREAMS[key] = torch.cuda.Stream(device)
+        self.copy = _COPY_STREAMS[key]
 
     def _issue(self, arena: Arena, items):
         torch = _torch()

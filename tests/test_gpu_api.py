@@ -353,3 +353,34 @@ def test_pinned_inputs_stream_bitwise(bri):
     sink = bri.MemorySink(prov.layout)
     bri.invert_full(prov, sink)
     assert np.abs(a @ sink.finalize() - np.eye(256)).max() <= 1e-9
+
+
+def test_concurrent_threads(bri):
+    """invert_block from several Python threads at once (the reference's
+    invert_full(jobs > 1) pattern, engine.py:343): every thread drives its own
+    context and arena; results equal the sequential ones bit for bit."""
+    import threading
+
+    import torch
+
+    a = shifted(512, 17)
+    prov = bri.make_memory_provider(a, 4)
+    targets = [(1, 1), (2, 3), (4, 2), (3, 4)]
+    want = {t: bri.invert_block(prov, *t).data for t in targets}
+    got, errors = {}, []
+
+    def work(t):
+        try:
+            got[t] = bri.invert_block(prov, *t).data
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in targets]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for t in targets:
+        np.testing.assert_array_equal(got[t], want[t])
