@@ -58,15 +58,9 @@ struct WarpAcc {
   // Consume one k-tile: A rows [wm0, wm0 + 16*MI), B cols [wn0, wn0 + 8*NJ).
   // Lanes whose k index is >= kvalid contribute zeros (K tail).
   BRI_DEVI void mma_stage(const uint8_t* sA, const uint8_t* sB, int kvalid, int wm0, int wn0, int lane) {
-    mma_stage_steps<0, 1>(sA, sB, kvalid, wm0, wn0, lane);
-  }
-
-  // Only the k4-steps KS0, KS0 + KSTRIDE, ... of the stage (k split across warp groups).
-  template <int KS0, int KSTRIDE>
-  BRI_DEVI void mma_stage_steps(const uint8_t* sA, const uint8_t* sB, int kvalid, int wm0, int wn0, int lane) {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-    for (int kk = KS0; kk < TILE_BK / 4; kk += KSTRIDE) {
+    for (int kk = 0; kk < TILE_BK / 4; ++kk) {
       const int k = kk * 4 + t;
       const bool kin = k < kvalid;
       double a[MI][2], bf[NJ];

@@ -114,8 +114,7 @@ template <bool LOWER, int BN, int STAGES>
 __global__ void __launch_bounds__(THREADS, 2)
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
   constexpr int SB = StageGeom<T, BN>::BYTES;
-  constexpr int NJ = BN / 8;        // n8 tiles per warp in the K loop (16 x BN per warp)
-  constexpr int XJ = BN / 16;       // n8 tiles per warp in the Tinv * R product
+  constexpr int XJ = BN / 16;       // n8 tiles per warp (4 warps along M x 2 along N, 16 x BN/2 each)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double* D = reinterpret_cast<double*>(smem + STAGES * SB);   // Tinv_ii, [k][m] col-major (LDD)
@@ -133,12 +132,9 @@ __global__ void __launch_bounds__(THREADS, 2)
   double* W = p.base + (long long)ws * p.slot_elems;
   const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
   const int nb = (p.nr + T - 1) / T;
-  // K loop: two warp groups split every stage's k4-steps (even / odd), each
-  // warp owning 16 rows x all 32 columns: four independent accumulator chains
-  // per warp keep the DMMA pipe fed; the halves are summed in smem.
-  const int kg = warp >> 2;
-  const int wm0 = (warp & 3) * 16;
-  // the Tinv * R product: 4 warps along M x 2 along N, 16 x 16 each
+  // both products: 4 warps along M x 2 along N, 16 x BN/2 each; every output
+  // element accumulates its k range in ascending k4-steps (splitting k across
+  // warps was measured no faster and changes the rounding near singular pivots)
   const int xm0 = (warp & 3) * 16, xn0 = (warp >> 2) * (BN / 2);
   const bool producer = (warp == 0 && lane == 0);
 
@@ -190,16 +186,13 @@ __global__ void __launch_bounds__(THREADS, 2)
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    WarpAcc<1, NJ> acc;
+    WarpAcc<1, XJ> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
       const int s = (it + kt) % STAGES;
       mbar_wait(&full[s], ((it + kt) / STAGES) & 1);
       const uint8_t* sA = smem + s * SB;
-      if (kg == 0)
-        acc.mma_stage_steps<0, 2>(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, 0, lane);
-      else
-        acc.mma_stage_steps<1, 2>(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, wm0, 0, lane);
+      acc.mma_stage(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, xm0, xn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (producer && kt >= 1) {
@@ -230,29 +223,16 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    // R = B_i - (acc_even + acc_odd)  (rows >= rows and columns >= nrhs are zero)
-    if (kg == 1) {
+    // R = B_i - acc  (rows >= rows and columns >= nrhs are zero)
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+    for (int j = 0; j < XJ; ++j)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int r = wm0 + g + ((v >> 1) << 3);
-          const int cc = j * 8 + 2 * t + (v & 1);
-          R[cc * LDR + r] = acc.c[0][j][v];
-        }
-    }
-    __syncthreads();
-    if (kg == 0) {
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int r = wm0 + g + ((v >> 1) << 3);
-          const int cc = j * 8 + 2 * t + (v & 1);
-          const bool ok = r < rows && c0 + cc < cend;
-          R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - (acc.c[0][j][v] + R[cc * LDR + r]) : 0.0;
-        }
-    }
+      for (int v = 0; v < 4; ++v) {
+        const int r = xm0 + g + ((v >> 1) << 3);
+        const int cc = xn0 + j * 8 + 2 * t + (v & 1);
+        const bool ok = r < rows && c0 + cc < cend;
+        R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - acc.c[0][j][v] : 0.0;
+      }
     __syncthreads();
     // X_i = Tinv_ii * R   (64 x BN x 64 DMMA from smem)
     double x[XJ][4];
