@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(THREADS, 2)
   constexpr int SB = StageGeom<T, BN>::BYTES;
   constexpr int XJ = BN / 16;       // n8 tiles per warp (4 warps along M x 2 along N, 16 x BN/2 each)
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (TMA 128B swizzle atoms) by pointer arithmetic on the
+  // __shared__ array, so the compiler keeps the shared address space (LDS, not
+  // generic LD with 64-bit address math) for every fragment load
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* D = reinterpret_cast<double*>(smem + STAGES * SB);   // Tinv_ii, [k][m] col-major (LDD)
   double* R = D + T * LDD;                                              // B_i - acc, [n][k] (LDR)
   double* Bst = R + BN * LDR;                                           // prefetched B_i, [n][k] (LDB)
