@@ -56,13 +56,15 @@ struct WarpAcc {
   }
 
   // Consume one k-tile: A rows [wm0, wm0 + 16*MI), B cols [wn0, wn0 + 8*NJ).
-  // Lanes whose k index is >= kvalid contribute zeros (K tail).
+  // Lanes whose k index is >= kvalid contribute zeros (K tail); FULL (a
+  // whole k-tile is valid) drops those predicates.
+  template <bool FULL = false>
   BRI_DEVI void mma_stage(const uint8_t* sA, const uint8_t* sB, int kvalid, int wm0, int wn0, int lane) {
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int kk = 0; kk < TILE_BK / 4; ++kk) {
       const int k = kk * 4 + t;
-      const bool kin = k < kvalid;
+      const bool kin = FULL || k < kvalid;
       double a[MI][2], bf[NJ];
 #if BRI_WIDE_A
       const uint32_t sw = (k & 7) << 4;

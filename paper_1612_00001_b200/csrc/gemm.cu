@@ -103,7 +103,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int s = kt % STAGES;
     mbar_wait(&full[s], (kt / STAGES) & 1);
     const uint8_t* sA = smem + s * STAGE_BYTES;
-    acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
+    if (p.K - kt * BK >= BK)
+      acc.template mma_stage<true>(sA, sA + StageGeom<BM, BN>::A_BYTES, BK, wm0, wn0, lane);
+    else
+      acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (producer && kt >= 1) {
@@ -219,6 +222,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int gg = g0 + kt, s = gg % STAGES;
       mbar_wait(&full[s], (gg / STAGES) & 1);
       const uint8_t* sA = smem + s * STAGE_BYTES;
+      if (p.K - kt * BK >= BK)
+      acc.template mma_stage<true>(sA, sA + StageGeom<BM, BN>::A_BYTES, BK, wm0, wn0, lane);
+    else
       acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(THREADS, 2)
       const int s = (it + kt) % STAGES;
       mbar_wait(&full[s], ((it + kt) / STAGES) & 1);
       const uint8_t* sA = smem + s * SB;
-      acc.mma_stage(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, xm0, xn0, lane);
+      if (K - kt * TILE_BK >= TILE_BK)
+        acc.template mma_stage<true>(sA, sA + StageGeom<T, BN>::A_BYTES, TILE_BK, xm0, xn0, lane);
+      else
+        acc.mma_stage(sA, sA + StageGeom<T, BN>::A_BYTES, K - kt * TILE_BK, xm0, xn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (producer && kt >= 1) {
