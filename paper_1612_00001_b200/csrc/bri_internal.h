@@ -28,7 +28,12 @@ constexpr int NBMAX = 32;        // LU panel width upper bound
 constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
 constexpr int TRSM_BLOCK = 64;   // diagonal block of the fused triangular solve
 constexpr int TRSM_LEAF = 512;
-constexpr int LU_OUTER = 128;   // outer block width of the two-level LU (multiple of TRSM_BLOCK and NBMAX)   // recursive solves hand sub-triangles up to this size to trsm.cu
+#ifndef BRI_LU_OUTER
+#define BRI_LU_OUTER 128
+#endif
+// outer block width of the two-level LU (multiple of TRSM_BLOCK and NBMAX); 256 measured
+// slower on config 2 (33.0 vs 32.4 ms) and equal on config 3
+constexpr int LU_OUTER = BRI_LU_OUTER;
 
 // Arena geometry: nslots column-major n x n blocks (X-world), leading dim ld
 // (multiple of 8, >= n), slot i at base + i * slot_elems.

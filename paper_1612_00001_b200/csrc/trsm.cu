@@ -42,9 +42,6 @@ BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
                "r"(valid ? 16 : 0)
                : "memory");
 }
-BRI_DEVI void cp_async_commit_wait() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
 
 // --------------------------------------------------------------- dinv
 // Invert the T x T diagonal blocks of the factor in slot F: unit lower (L) or
