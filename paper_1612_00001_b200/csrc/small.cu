@@ -22,14 +22,29 @@ namespace {
 
 constexpr int SN_THREADS = 256;
 
+#ifdef BRI_SMALL_PROFILE
+__device__ unsigned long long g_small_phase[8];
+#define SPROF(k)                                                   \
+  do {                                                             \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                     \
+      const unsigned long long now = clock64();                    \
+      atomicAdd(&g_small_phase[k], now - t_last);                  \
+      t_last = now;                                                \
+    }                                                              \
+  } while (0)
+#else
+#define SPROF(k) do { } while (0)
+#endif
+
 template <int NMAX>
 __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, const int* items, int mode,
                                                                 int* status) {
   constexpr int LDS = NMAX + 1;
+  constexpr int LDW = NMAX + 8;    // W rows: 8 columns x 4 rows per warp access hit 2 wavefronts
   extern __shared__ double sm[];
   double* F = sm;                  // factor of p^   (F[c * LDS + i] = element (i, c))
-  double* W = F + NMAX * LDS;      // right-hand side / solution
-  double* RT = W + NMAX * LDS;     // rt^ (mode 0 only)
+  double* RT = F + NMAX * LDS;     // rt^ (mode 0 only)
+  double* W = RT + NMAX * LDS;     // right-hand side / solution, row-major: W[i * LDW + c]
   __shared__ int perm[NMAX];
   __shared__ int piv_s;
   __shared__ unsigned long long scale_bits;
@@ -44,6 +59,9 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
   double* Out = a.base + (long long)it[4] * a.slot_elems;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+#ifdef BRI_SMALL_PROFILE
+  unsigned long long t_last = clock64();
+#endif
   if (tid == 0) {
     scale_bits = 0ull;
     first_bad = INT_MAX;
@@ -67,6 +85,7 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
   if (lane == 0) atomicMax(&scale_bits, (unsigned long long)__double_as_longlong(mx));
   __syncthreads();
 
+  SPROF(0);
   // ------------------------------------------------ dgetf2 on F (in smem)
   for (int j = 0; j < n; ++j) {
     if (warp == 0) {
@@ -102,14 +121,15 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
       }
     }
     __syncthreads();
-    const int m = n - j - 1;
-    for (int e = tid; e < m * m; e += SN_THREADS) {
-      const int i = j + 1 + e % m, c = j + 1 + e / m;
-      F[c * LDS + i] = fma(-F[j * LDS + i], F[c * LDS + j], F[c * LDS + i]);
+    // rank-1 update, one warp per column (no index division, coalesced rows)
+    for (int c = j + 1 + warp; c < n; c += SN_THREADS / 32) {
+      const double u = F[c * LDS + j];
+      for (int i = j + 1 + lane; i < n; i += 32) F[c * LDS + i] = fma(-F[j * LDS + i], u, F[c * LDS + i]);
     }
     __syncthreads();
   }
 
+  SPROF(1);
   // ------------------------------------------------ singularity test
   {
     const double tol = (double)n * kEps * __longlong_as_double((long long)scale_bits);
@@ -123,27 +143,45 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
   for (int e = tid; e < n * n; e += SN_THREADS) {
     const int x = e % n, c = e / n;
     const int s = perm[x];
-    W[c * LDS + x] = (mode == 1) ? (s == c ? 1.0 : 0.0) : Lb[s + (long long)c * ld];
+    W[x * LDW + c] = (mode == 1) ? (s == c ? 1.0 : 0.0) : Lb[s + (long long)c * ld];
   }
   __syncthreads();
-  for (int c = tid; c < n; c += SN_THREADS) {
-    double* w = W + c * LDS;
+  SPROF(2);
+  // Forward (unit L) and backward (U) substitution, TPC threads per right-hand
+  // side column (one warp holds 32 / TPC columns): each step's row updates are
+  // split between them and a __syncwarp orders the steps.  Every element sees
+  // the column-serial operation sequence (fma(-x_k, L_ik, w_i) for k ascending;
+  // x_k = w_k / U_kk, then fma(-x_k, U_ik, w_i) for k descending).
+  {
+    constexpr int TPC = (SN_THREADS / NMAX) >= 8 ? 8 : (SN_THREADS / NMAX) >= 4 ? 4 : 2;
+    const int c = tid / TPC, part = tid % TPC;
+    double* w = W + c;               // element i of this column at w[i * LDW]
+    const bool col = c < n;
     for (int k = 0; k < n; ++k) {
-      const double xk = w[k];
-      for (int i = k + 1; i < n; ++i) w[i] = fma(-xk, F[k * LDS + i], w[i]);
+      if (col) {
+        const double xk = w[k * LDW];
+        for (int i = k + 1 + part; i < n; i += TPC) w[i * LDW] = fma(-xk, F[k * LDS + i], w[i * LDW]);
+      }
+      __syncwarp();
     }
     for (int k = n - 1; k >= 0; --k) {
-      const double xk = w[k] / F[k * LDS + k];
-      w[k] = xk;
-      for (int i = 0; i < k; ++i) w[i] = fma(-xk, F[k * LDS + i], w[i]);
+      double xk = 0.0;
+      if (col) xk = w[k * LDW] / F[k * LDS + k];
+      __syncwarp();
+      if (col) {
+        if (part == 0) w[k * LDW] = xk;
+        for (int i = part; i < k; i += TPC) w[i * LDW] = fma(-xk, F[k * LDS + i], w[i * LDW]);
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
 
+  SPROF(3);
   if (mode == 1) {
     for (int e = tid; e < n * n; e += SN_THREADS) {
       const int i = e % n, c = e / n;
-      Out[i + (long long)c * ld] = W[c * LDS + i];
+      Out[i + (long long)c * ld] = W[i * LDW + c];
     }
     return;
   }
@@ -162,7 +200,7 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
 #pragma unroll
       for (int u = 0; u < 4; ++u) ra[u] = (i0 + u < n) ? RT[k * LDS + i0 + u] : 0.0;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) wb[v] = (c0 + v < n) ? W[(c0 + v) * LDS + k] : 0.0;
+      for (int v = 0; v < 4; ++v) wb[v] = (c0 + v < n) ? W[k * LDW + c0 + v] : 0.0;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -179,12 +217,16 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
         }
       }
   }
+  SPROF(4);
 }
+
+template <int NMAX>
+constexpr int small_smem() { return (2 * NMAX * (NMAX + 1) + NMAX * (NMAX + 8)) * 8; }
 
 template <int NMAX>
 cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int mode, int* status,
                            cudaStream_t s) {
-  const int smem = 3 * NMAX * (NMAX + 1) * 8;
+  const int smem = small_smem<NMAX>();
   count_launch();
   small_node_kernel<NMAX><<<count, SN_THREADS, smem, s>>>(a, items, mode, status);
   return cudaGetLastError();
@@ -192,14 +234,22 @@ cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int 
 
 }  // namespace
 
+#ifdef BRI_SMALL_PROFILE
+void small_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_small_phase, sizeof(g_small_phase));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_small_phase, z, sizeof(z));
+}
+#endif
+
 cudaError_t configure_small() {
   cudaError_t e = cudaFuncSetAttribute(small_node_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       3 * 32 * 33 * 8);
+                                       small_smem<32>());
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(small_node_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 64 * 65 * 8);
+    e = cudaFuncSetAttribute(small_node_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem<64>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(small_node_kernel<SMALL_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             3 * SMALL_MAX * (SMALL_MAX + 1) * 8);
+                             small_smem<SMALL_MAX>());
   return e;
 }
 
