@@ -175,7 +175,7 @@ BRI_DEVI void store_live_row(double* dst, const double (&x)[RPT][PNB], int q) {
   }
   dst[1] = r[0];
 #pragma unroll
-  for (int c = 1; c < PNB - 1; c += 2) sts_f64x2(&dst[c + 1], r[c], r[c + 1]);
+  for (int c = 1; c < PNB - 1; c += 2) *reinterpret_cast<double2*>(&dst[c + 1]) = make_double2(r[c], r[c + 1]);
   dst[PNB] = r[PNB - 1];
 }
 
@@ -312,8 +312,10 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
     // ---- (4) interchange, scale, rank-1 update
     const bool none = gp == INT_MAX;      // no comparable value in the column: pivot in place
     const int pr = none ? j : gp;
-    const uint32_t aS = smem_u32(win->S);
-    const double piv = none ? kNaN : lds_f64(aS + 8);
+    // plain shared loads through the message pointer: immediate offsets, no
+    // per-load address math (the waits above are compiler memory barriers)
+    const double* wS = win->S;
+    const double piv = none ? kNaN : wS[1];
     if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
     const bool swap = (pr != j && piv != 0.0);  // dgetf2 interchanges only for a nonzero pivot
     const bool recip = fabs(piv) >= kSfmin;
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
       const unsigned fm = __ballot_sync(0xffffffffu, fast_slot >= 0);
       if (fm) {
         const int slot = __shfl_sync(0xffffffffu, fast_slot, __ffs(fm) - 1);
-        if (lane < nb - jj) psm[(jj + lane) * rhp + slot] = lds_f64(aS + 8 * (lane + 1));
+        if (lane < nb - jj) psm[(jj + lane) * rhp + slot] = wS[lane + 1];
       }
     }
     PPROF(4);
@@ -352,7 +354,11 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
       for (int c = 0; c < PNB; ++c) u[c] = kNaN;
     } else {
 #pragma unroll
-      for (int c = 0; c < PNB; c += 2) lds_f64x2(aS + 16 + 8 * c, u[c], u[c + 1]);
+      for (int c = 0; c < PNB; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(&wS[c + 2]);
+        u[c] = v.x;
+        u[c + 1] = v.y;
+      }
     }
     double nl[RPT];
 #pragma unroll
