@@ -74,6 +74,7 @@ struct LuScratch {
   int* pairs;     // npanels * (1 + 2 * NBMAX)
   unsigned long long* scale_bits;  // 1 (max |X| as double bits)
   int* status;    // 1
+  int* orig;      // n   (tall panels: original row now at each position)
 };
 
 cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
@@ -87,7 +88,8 @@ cudaError_t launch_colscatter(const ArenaView& a, const int* pairs, int count, c
                               cudaStream_t s);
 cudaError_t launch_identity(const ArenaView& a, const int* slots, int slot_stride, int count, cudaStream_t s);
 int panel_width(int n);
-int max_panel_rows();  // largest order the register-resident panel factors (16-CTA cluster, 2 rows/thread)
+int max_panel_rows();  // largest order the register-resident panel factors (16-CTA cluster, 2 rows/thread);
+                       // taller panels go through the global-memory tall-panel kernel
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                          const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
 cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,

@@ -119,7 +119,7 @@ int upload(bri_ctx* ctx, cudaStream_t s, const std::vector<int>& h, int** dev) {
 
 struct LuLayout {
   int n, count, npanels, pair_stride;
-  size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, total;
+  size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, off_orig, total;
 };
 
 LuLayout lu_layout(int n, int count) {
@@ -141,6 +141,7 @@ LuLayout lu_layout(int n, int count) {
   L.off_pairs = take((size_t)count * L.pair_stride * 4);
   L.off_scale = take((size_t)count * 8);
   L.off_status = take((size_t)count * 4);
+  L.off_orig = take((size_t)count * n * 4);
   L.total = off;
   return L;
 }
@@ -154,6 +155,7 @@ LuScratch lu_scratch(void* base, const LuLayout& L) {
   s.pairs = reinterpret_cast<int*>(b + L.off_pairs);
   s.scale_bits = reinterpret_cast<unsigned long long*>(b + L.off_scale);
   s.status = reinterpret_cast<int*>(b + L.off_status);
+  s.orig = reinterpret_cast<int*>(b + L.off_orig);
   return s;
 }
 
@@ -639,9 +641,6 @@ int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, in
                     int* status) {
   if (ar == nullptr || slots == nullptr || count < 0) return fail_msg("bri_getrf_batch: bad arguments");
   if (count == 0) return 0;
-  if (ar->v.n > max_panel_rows())
-    return fail_msg("bri_getrf_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
-                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   std::vector<int> h(7 * (size_t)count);
@@ -687,9 +686,6 @@ int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, co
 int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_invert_batch: bad arguments");
   if (count == 0) return 0;
-  if (ar->v.n > max_panel_rows())
-    return fail_msg("bri_invert_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
-                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   if (n <= SMALL_MAX) {
@@ -761,9 +757,6 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
                           void* ev_rtr) {
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_schur_batch: bad arguments");
   if (count == 0) return 0;
-  if (ar->v.n > max_panel_rows())
-    return fail_msg("bri_schur_batch: block order " + std::to_string(ar->v.n) + " exceeds the LU panel limit " +
-                    std::to_string(max_panel_rows()));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   auto I = [&](int i, int k) { return items[7 * i + k]; };  // p, rt, l, r, out, f, w

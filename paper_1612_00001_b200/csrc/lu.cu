@@ -428,6 +428,130 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
 }
 
 
+
+// ------------------------------------------------------------- tall panel
+// Panels taller than the register-resident kernel holds (n - j0 > 8192, e.g.
+// b = 20480 of BASELINE config 5): the same dgetf2 decisions with the panel
+// kept in global memory (L2-resident: 32 columns x n rows), one 16-CTA cluster
+// per factor.  Per column: strided argmax -> warp/CTA/cluster reduction
+// (DSMEM stores + cluster barrier) -> physical swap of rows j and p (one
+// thread per panel column) -> scale + rank-1 update of the remaining panel
+// columns, every thread on its rows.  Three cluster barriers per column;
+// slower than the register kernel but unbounded in height.
+constexpr int TALL_CS = 16;
+
+struct TallArgs {
+  ArenaView a;
+  const int* slots;
+  int j0, nb, pidx;
+  int* ipiv;
+  int* sigma;
+  int* pairs;
+  int* orig;
+  int n_stride, pair_stride;
+};
+
+__global__ void __launch_bounds__(PT, 1) lu_panel_tall_kernel(TallArgs p) {
+  __shared__ double wv[PW];
+  __shared__ int wi[PW];
+  __shared__ double cv[TALL_CS];
+  __shared__ int ci[TALL_CS];
+  __shared__ int prow;
+  const int cs = (int)cluster_nctarank();
+  const int rank = (int)cluster_ctarank();
+  const int item = blockIdx.x / cs;
+  const int n = p.a.n, ld = p.a.ld, nb = p.nb, j0 = p.j0;
+  double* X = p.a.base + (long long)p.slots[item] * p.a.slot_elems;
+  int* orig = p.orig + (long long)item * p.n_stride;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gtid = rank * PT + tid, gthreads = cs * PT;
+  for (int i = j0 + gtid; i < n; i += gthreads) orig[i] = i;
+  cluster_sync_all();
+  for (int jj = 0; jj < nb; ++jj) {
+    const int j = j0 + jj;
+    double* colj = X + (long long)j * ld;        // X-column j = one memory row
+    // ---- argmax |X(i, j)| over i >= j (NaN never wins, smallest index on ties)
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int i = j + gtid; i < n; i += gthreads) {
+      const double v = fabs(colj[i]);
+      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+    }
+    warp_argmax_fast(bv, bi);
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      double v = wv[lane % PW];
+      int i = wi[lane % PW];
+      warp_argmax_fast(v, i);
+      if (lane < cs) {   // our CTA's candidate into slot `rank` of every CTA
+        const uint32_t a = dsmem_addr(&cv[rank], lane), b = dsmem_addr(&ci[rank], lane);
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+        asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(b), "r"(i) : "memory");
+      }
+    }
+    cluster_sync_all();
+    if (warp == 0) {
+      double v = lane < cs ? cv[lane] : -1.0;
+      int i = lane < cs ? ci[lane] : INT_MAX;
+      warp_argmax_fast(v, i);
+      if (lane == 0) prow = (i == INT_MAX) ? j : i;   // all NaN: pivot in place
+    }
+    __syncthreads();
+    const int pr = prow;
+    const double piv = colj[pr];
+    if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
+    const bool swap = (pr != j && piv != 0.0);
+    if (swap && rank == 0) {
+      if (tid < nb) {
+        double* col = X + (long long)(j0 + tid) * ld;
+        const double t = col[j];
+        col[j] = col[pr];
+        col[pr] = t;
+      } else if (tid == nb) {
+        const int t = orig[j];
+        orig[j] = orig[pr];
+        orig[pr] = t;
+      }
+    }
+    cluster_sync_all();   // the interchange is visible cluster-wide (release / acquire)
+    // ---- scale and rank-1 update of columns jj+1.. on rows i > j
+    const bool recip = fabs(piv) >= kSfmin;
+    const double rinv = 1.0 / piv;
+    double u[NBMAX];   // the pivot row's remaining panel entries (same for every row)
+#pragma unroll
+    for (int c = 0; c < NBMAX; ++c) u[c] = (c > jj && c < nb) ? X[(long long)(j0 + c) * ld + j] : 0.0;
+    for (int i = j + 1 + gtid; i < n; i += gthreads) {
+      double l = colj[i];
+      if (piv != 0.0) {
+        l = recip ? l * rinv : l / piv;
+        colj[i] = l;
+      }
+      double v[NBMAX];   // all loads of the row first: one L2 round trip, not one per column
+#pragma unroll
+      for (int c = 0; c < NBMAX; ++c)
+        if (c > jj && c < nb) v[c] = X[(long long)(j0 + c) * ld + i];
+#pragma unroll
+      for (int c = 0; c < NBMAX; ++c)
+        if (c > jj && c < nb) X[(long long)(j0 + c) * ld + i] = fma(-l, u[c], v[c]);
+    }
+    cluster_sync_all();   // column jj+1 is final before its argmax
+  }
+  // position P in [j0, n) now holds original row orig[P]
+  int* sig = p.sigma + (long long)item * p.n_stride;
+  int* pairs = p.pairs + (long long)item * p.pair_stride + (long long)p.pidx * (1 + 2 * NBMAX);
+  for (int P = j0 + gtid; P < n; P += gthreads) {
+    const int g = orig[P];
+    if (P < j0 + nb) {
+      sig[P] = g;
+    } else if (g != P) {
+      const int k = atomicAdd(pairs, 1);
+      pairs[1 + 2 * k] = P;
+      pairs[2 + 2 * k] = g;
+    }
+  }
+}
+
 // --------------------------------------------------------------- rowpanel
 // One warp per X-column outside the panel (a contiguous memory row): apply
 // the panel's interchanges as a gather (all reads before any write, ordered
@@ -642,6 +766,7 @@ cudaError_t configure_lu() {
     e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_tall_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
@@ -656,10 +781,25 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   // (one row per thread on a 16-CTA cluster is faster alone at 4096 rows — 1.70
   // vs 1.87 us/column — but a 16-SM cluster waits for SMs next to the
   // concurrent trailing update: config 2 went from 35.0 to 39.4 ms)
+  if (h > max_panel_rows()) {
+    TallArgs t{a, slots, j0, nb, pidx, sc.ipiv, sc.sigma, sc.pairs, sc.orig, n_stride, pair_stride};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(count * TALL_CS);
+    cfg.blockDim = dim3(PT);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = TALL_CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, lu_panel_tall_kernel, t);
+  }
   const int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
   int cs = 1;
   while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
-  if ((h + cs - 1) / cs > rpt * PT) return cudaErrorInvalidValue;  // order > max_panel_rows()
   PanelArgs p;
   p.a = a;
   p.slots = slots;

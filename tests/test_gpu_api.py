@@ -322,9 +322,10 @@ def test_dense_lu_baseline_and_verify(bri, golden, tmp_path):
         baseline.verify(a, inverse=np.eye(3))
 
 
-@pytest.mark.parametrize("n", [4097, 6144, 8192])
+@pytest.mark.parametrize("n", [4097, 6144, 8192, 12288])
 def test_dense_inverse_tall_panels(bri, n):
-    """Orders above 4096 factor their panels on 16-CTA (non-portable) clusters."""
+    """Orders above 4096 factor their panels on 16-CTA (non-portable) clusters; above 8192
+    rows the panel lives in global memory (lu_panel_tall_kernel)."""
     import torch
 
     from paper_1612_00001_b200 import baseline
@@ -384,3 +385,15 @@ def test_concurrent_threads(bri):
     assert not errors, errors
     for t in targets:
         np.testing.assert_array_equal(got[t], want[t])
+
+
+def test_tall_block_node_matches_oracle(bri):
+    """A Schur node of order 10240 (BASELINE config 5's regime, b > 8192): tall panels in both
+    factorizations, checked against the CPU oracle (the reference's LAPACK calls)."""
+    from conftest import rel_err
+    from oracle import bri_oracle as orc
+
+    a = shifted(20480, 41)
+    got = bri.invert_block(bri.make_memory_provider(a, 2), 1, 1).data
+    ref = orc.invert_block(a, 2, 1, 1)
+    assert rel_err(got, ref) <= 1e-9
