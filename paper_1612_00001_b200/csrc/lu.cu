@@ -25,6 +25,8 @@
 #include "bri_common.cuh"
 #include "bri_internal.h"
 
+#include <cstdlib>
+
 namespace bri {
 
 namespace {
@@ -797,7 +799,18 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
     count_launch();
     return cudaLaunchKernelEx(&cfg, lu_panel_tall_kernel, t);
   }
-  const int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
+  // Large batches run in many waves of one CTA per SM (registers bound the rows
+  // resident per SM), so beyond two waves two rows per thread halves the waves
+  // (config 3: 1.60 -> 1.52 s).
+  static const int wide_waves = [] {
+    const char* e = getenv("BRI_PANEL_RPT2_WAVES");
+    return e ? atoi(e) : 2;
+  }();
+  int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
+  if (rpt == 1 && h > PT) {
+    const long long ctas1 = (long long)count * ((h + PT - 1) / PT);
+    if (ctas1 > (long long)wide_waves * 148) rpt = 2;
+  }
   int cs = 1;
   while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
   PanelArgs p;
