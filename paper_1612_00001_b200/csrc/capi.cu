@@ -807,19 +807,19 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
   BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
   if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc)) return rc;
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
-  if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), 0));
+  if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
   BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
   if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count, false, true)) return rc;
-  if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), 0));
+  if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
   return gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
   };
-  // gated runs wait on input copies still in flight: issued directly (a graph
-  // would freeze the events), everything else replays a captured graph
-  if (ev_l || ev_rtr) {
-    if (int rc = issue(s)) return rc;
-  } else if (int rc = run_graphed(ar->ctx, s, graph_key(0, ar, count, dev), issue)) {
-    return rc;
-  }
+  // gated runs wait on input copies still in flight through external event
+  // nodes of the captured graph: the caller records the same (persistent)
+  // events before every launch, so the graph keyed on them replays
+  std::vector<uintptr_t> key = graph_key(0, ar, count, dev);
+  key.push_back((uintptr_t)ev_l);
+  key.push_back((uintptr_t)ev_rtr);
+  if (int rc = run_graphed(ar->ctx, s, key, issue)) return rc;
   if (status) BRI_CHECK(cudaMemcpyAsync(status, sc.status, (size_t)count * 4, cudaMemcpyDeviceToDevice, s));
   return 0;
 }

@@ -123,32 +123,33 @@ class _PinnedSource:
     run needs are copied host -> slot (2-D async copies) on a dedicated copy
     stream, in the order the run first reads them.  `load` makes the caller's
     stream wait for its copies; `load_gated` instead returns events so a DAG
-    level can factor its pivots while the other operands are still in flight."""
+    level can factor its pivots while the other operands are still in flight.
+    The events are persistent per device and thread (re-recorded every run), so
+    the gated schur graph captured on them replays."""
 
     def __init__(self, pinned, b: int, device: int):
         torch = _torch()
         self.t, self.b, self.device = pinned, b, device
         key = (device, threading.get_ident())
         if key not in _COPY_STREAMS:
-            _COPY_STREAMS[key] = torch.cuda.Stream(device)
-        self.copy = _COPY_STREAMS[key]
+            _COPY_STREAMS[key] = (torch.cuda.Stream(device), [torch.cuda.Event() for _ in range(4)])
+        self.copy, self.events = _COPY_STREAMS[key]
 
-    def _issue(self, arena: Arena, items):
+    def _issue(self, arena: Arena, items, ev):
         torch = _torch()
         self.copy.wait_stream(torch.cuda.current_stream(self.device))   # slots may have been in use
         arena.load_host(self.t, [(i - 1, j - 1, s) for i, j, s in items], stream=self.copy)
-        ev = torch.cuda.Event()
         ev.record(self.copy)
         return ev
 
     def load(self, arena: Arena, items) -> None:
         items = list(items)
         if items:
-            _torch().cuda.current_stream(self.device).wait_event(self._issue(arena, items))
+            _torch().cuda.current_stream(self.device).wait_event(self._issue(arena, items, self.events[3]))
 
     def load_gated(self, arena: Arena, groups):
-        """groups: item lists in first-use order; returns one event per group."""
-        return [self._issue(arena, g) if g else None for g in groups]
+        """groups: item lists in first-use order (at most 3); returns one event per group."""
+        return [self._issue(arena, g, self.events[q]) if g else None for q, g in enumerate(groups)]
 
 
 class _WindowSource:
