@@ -27,7 +27,11 @@ cudaError_t configure_trsm();
 constexpr int NBMAX = 32;        // LU panel width upper bound
 constexpr int SMALL_MAX = 96;    // blocks up to this order run the fused one-CTA kernels
 constexpr int TRSM_BLOCK = 64;   // diagonal block of the fused triangular solve
-constexpr int TRSM_LEAF = 512;
+#ifndef BRI_TRSM_LEAF
+#define BRI_TRSM_LEAF 512
+#endif
+constexpr int TRSM_LEAF = BRI_TRSM_LEAF;   // recursive solves hand sub-triangles up to this size to trsm.cu
+                                           // (256 and 1024 measured no better on configs 2 and 3)
 #ifndef BRI_LU_OUTER
 #define BRI_LU_OUTER 128
 #endif
