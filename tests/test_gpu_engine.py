@@ -174,3 +174,32 @@ def test_config4_singular_pivot_matches_reference():
         bri.invert_blocks(prov, cfg["targets"])
     assert "/".join(q.name for q in exc.value.path) == "A/D/A/D"
     assert tuple(exc.value.pivot_block) == (2, 2)
+
+
+def test_bounded_arena_groups_targets():
+    """A DAG that does not fit the arena budget is split into target groups
+    (engine._run_grouped); results equal the unbounded run bit for bit, the
+    device footprint stays under the budget, and a single target that cannot
+    fit raises BadPartitionError."""
+    import torch
+
+    import paper_1612_00001_b200 as bri
+    from paper_1612_00001_b200.dag import build_schedule
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = shifted(1024, 29)
+    prov = bri.make_memory_provider(a, 8)           # b = 128
+    targets = [(al, be) for al in range(1, 9) for be in range(1, 9)]
+    need = lambda tg: len(build_schedule(8, tg).m_blocks_used()) + build_schedule(8, tg).peak_level_blocks()
+    budget = need(targets[:8]) + 40                 # room for a group of 8 targets, not for all 64
+    assert need(targets) > budget
+    full, _ = bri.invert_blocks(prov, targets)
+    block = 128 * 128 * 8
+    ws = bri.Workspace(arena_bytes=budget * block)
+    part, info = bri.invert_blocks(prov, targets, ws)
+    assert ws.gauge.peak_blocks <= budget
+    for x, y in zip(full, part):
+        assert torch.equal(x, y)
+    with pytest.raises(bri.BadPartitionError):
+        bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=(need([(1, 1)]) - 10) * block))
