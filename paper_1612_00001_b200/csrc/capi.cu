@@ -87,7 +87,7 @@ struct bri_ctx {
   int device = 0;
   cudaStream_t side = nullptr;    // lookahead: bulk trailing updates of the LU
   cudaStream_t gstream = nullptr; // graphs are captured / launched here
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_in = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_x = nullptr, ev_in = nullptr, ev_out = nullptr;
   std::vector<GraphEntry> graphs; // captured hot-path sequences (LRU, <= 16)
   std::vector<std::vector<uintptr_t>> seen;
   DevBuf items;   // uploaded item arrays
@@ -186,12 +186,18 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
 // Blocked right-looking LU (dgetrf) of `count` slots in place, two levels
 // with lookahead:
 //   * outer blocks of 128 columns, each factored by 32-wide inner panels
-//     (cluster panel kernel + in-block rowpanel + rank-32 GEMM);
-//   * after block J is factored, its interchanges / U12 solve / rank-128
-//     update are applied FIRST to the next block's 128 columns on the caller's
-//     stream, which then factors that next block at once, while the same
-//     update of all remaining columns runs concurrently on the side stream.
-//     The pivot chain (panels) therefore overlaps the bulk trailing GEMMs.
+//     (cluster panel kernel + rowpanel + rank-32 GEMM);
+//   * batches of <= 2 (panel chain = critical path): the inner panels of
+//     block J also carry the NEXT block's 128 columns (interchanges, 32-row
+//     solve and rank-32 update per inner panel), so block J+1 is ready the
+//     moment block J's last panel finishes; meanwhile the side stream applies
+//     block J's interchanges / U12 solve / rank-128 update to block J+2's
+//     columns first (an event the main stream waits on before its own inner
+//     panels reach them), then to everything else;
+//   * larger batches: block J's update is applied first to block J+1's
+//     columns on the caller's stream, which then factors block J+1 while the
+//     side stream updates everything else.
+//   Either way the pivot chain (panels) overlaps the bulk trailing GEMMs.
 // dev_slots: F slots; dev_ffff: (F, F, F, F) quads; dev_ff: (F, F) pairs.
 int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, const int* dev_ff,
                  int count, const LuLayout& L, const LuScratch& sc) {
@@ -209,13 +215,17 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   if (int rc = ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
   double* dl = static_cast<double*>(ctx->dinv.ptr);
 
-  // factor the outer block [J0, J0 + W) whose columns are up to date (stream s)
-  auto factor_block = [&](int J0, int W, int pidx) -> int {
+  // factor the outer block [J0, J0 + W) whose columns are up to date (stream s),
+  // carrying every inner panel's interchanges / solve / update on to columns
+  // [J0 + W, cext) as well; `ext_ready`: event to wait on before the first of
+  // those touches [J0 + W, cext) (nullptr: already up to date)
+  auto factor_block = [&](int J0, int W, int pidx, int cext, cudaEvent_t ext_ready) -> int {
     for (int j0 = J0; j0 < J0 + W; j0 += nbi, ++pidx) {
       const int w = (J0 + W - j0) < nbi ? (J0 + W - j0) : nbi;
       BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
-      BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, J0 + W, sc, n, L.pair_stride, s));
-      const int right = J0 + W - j0 - w;
+      if (j0 == J0 && ext_ready) BRI_CHECK(cudaStreamWaitEvent(s, ext_ready, 0));
+      BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, cext, sc, n, L.pair_stride, s));
+      const int right = cext - j0 - w;
       if (right > 0 && n - j0 - w > 0) {
         if (int rc = gemm_call(ar, s, dev_ffff, count, n - j0 - w, right, w, j0 + w, j0, j0, j0 + w, j0 + w,
                                j0 + w, -1.0, 1.0))
@@ -248,33 +258,63 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     const char* e = getenv("BRI_LOOKAHEAD");
     return e == nullptr || e[0] != '0';
   }();
-  if (int rc = factor_block(0, n < outer ? n : outer, 0)) return rc;
+  // Extending the inner panels into the next block trades rank-128 GEMM work
+  // for rank-32 work: a win when the panel chain is the critical path (few
+  // factorizations: config 2 32.5 -> 31.4 ms/step), a loss when a large batch
+  // keeps every SM busy anyway (config 3 1.52 -> 1.57 s).
+  static const int extend_env = [] {
+    const char* e = getenv("BRI_LU_EXTEND");
+    return e ? atoi(e) : -1;
+  }();
+  const bool extend = lookahead && (extend_env >= 0 ? extend_env != 0 : count <= 2);
+  const int W0 = n < outer ? n : outer;
+  const int ext0 = extend ? (n < 2 * outer ? n : 2 * outer) : W0;
+  if (int rc = factor_block(0, W0, 0, ext0, nullptr)) return rc;
   for (int J0 = 0, pidx0 = 0; J0 < n; J0 += outer, pidx0 += npan_outer) {
     const int W = (n - J0) < outer ? (n - J0) : outer;
     const int npan = (W + nbi - 1) / nbi;
     const int N0 = J0 + W;
     const int WN = (n - N0) < outer ? (n - N0) : outer;
+    const int N1 = N0 + WN;
+    const int WNN = (n - N1) < outer ? (n - N1) : outer;
     if ((J0 % TRSM_BLOCK) != 0) return fail_msg("getrf: outer block not aligned to the TRSM block");
     if (WN > 0 && !lookahead) {
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N0, n, sc, n,
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
       if (int rc = update_cols(s, J0, W, pidx0, N0, n, 0)) return rc;
-      if (int rc = factor_block(N0, WN, pidx0 + npan_outer)) return rc;
-    } else if (WN > 0) {
+      if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
+    } else if (WN > 0 && !extend) {
       // critical path: next block's columns, then factor it
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, N0, N0 + WN, 0, 0, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, N0, N1, 0, 0, sc, n,
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
       BRI_CHECK(cudaEventRecord(ctx->ev_a, s));
-      if (int rc = update_cols(s, J0, W, pidx0, N0, N0 + WN, 0)) return rc;
+      if (int rc = update_cols(s, J0, W, pidx0, N0, N1, 0)) return rc;
       // bulk: everything else, concurrently on the side stream
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N0 + WN, n, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N1, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N0 + WN, n, trail_cap)) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N1, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
-      if (int rc = factor_block(N0, WN, pidx0 + npan_outer)) return rc;
+      if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
+      BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
+    } else if (WN > 0) {
+      // block J (and, through its inner panels, block J+1's columns) is done
+      BRI_CHECK(cudaEventRecord(ctx->ev_a, s));
+      BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
+      BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s1));
+      if (WNN > 0) {   // block J+2's columns first: block J+1's inner panels extend into them
+        BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, N1, N1 + WNN, 0, 0, sc, n,
+                               L.pair_stride, s1));
+        if (int rc = update_cols(s1, J0, W, pidx0, N1, N1 + WNN, 0)) return rc;
+        BRI_CHECK(cudaEventRecord(ctx->ev_x, s1));
+      }
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N1 + WNN, n, sc, n,
+                             L.pair_stride, s1));
+      if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, trail_cap)) return rc;
+      BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
+      if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1 + WNN, WNN > 0 ? ctx->ev_x : nullptr)) return rc;
       BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     } else {
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, 0, 0, sc, n,
@@ -525,6 +565,7 @@ int bri_ctx_create(int device, bri_ctx** out) {
   BRI_CHECK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_low));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
+  BRI_CHECK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
   BRI_CHECK(cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, prio_high));
@@ -545,6 +586,7 @@ void bri_ctx_destroy(bri_ctx* ctx) {
   if (ctx->ev_out) cudaEventDestroy(ctx->ev_out);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
   delete ctx;
 }
 

@@ -397,3 +397,31 @@ def test_tall_block_node_matches_oracle(bri):
     got = bri.invert_block(bri.make_memory_provider(a, 2), 1, 1).data
     ref = orc.invert_block(a, 2, 1, 1)
     assert rel_err(got, ref) <= 1e-9
+
+
+@pytest.mark.parametrize("env", [{"BRI_LOOKAHEAD": "0"}, {"BRI_LU_EXTEND": "0"}, {"BRI_LU_EXTEND": "1"}])
+def test_lu_schedules_agree(bri, env, tmp_path):
+    """The three LU schedules (no lookahead; lookahead; lookahead with inner panels
+    extended into the next outer block, the default for batches of <= 2) each give the
+    dense inverse and the BRI blocks as accurately as the default schedule (errors against
+    numpy's LAPACK inverse; the BRI pivot blocks are poorly conditioned on purpose, so
+    schedules that round differently differ by far more than 1 ulp there)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    root = os.path.dirname(here)
+
+    def run(extra, name):
+        path = str(tmp_path / name)
+        e = dict(os.environ, PYTHONPATH=root, **extra)
+        subprocess.run([sys.executable, os.path.join(here, "_lu_schedules.py"), path], env=e, check=True,
+                       timeout=300)
+        return np.load(path)
+
+    ref, got = run({}, "ref.npz"), run(env, "got.npz")
+    for key in ref.files:
+        if key.startswith("err_"):
+            assert got[key] <= 4 * ref[key] + 1e-13, (key, float(got[key]), float(ref[key]), env)
+    assert rel_err(got["dense"], ref["dense"]) <= 1e-9

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 from scipy.linalg import lapack
 
-from conftest import rng, shifted
+from conftest import rel_err, rng, shifted
 
 pytestmark = pytest.mark.gpu
 
@@ -157,7 +157,9 @@ def test_batched_matches_single(torch_cuda):
     st = torch.zeros(cnt, dtype=torch.int32, device="cuda")
     ar.schur(items, st)
     batched = [ar.view(it[4]).cpu().numpy().copy() for it in items]
+    # a lone factorization takes the extended-panel LU schedule (batches of <= 2,
+    # capi.cu getrf_device), which rounds differently from the batched one
     for i, it in enumerate(items):
         ar.schur([it], st[:1])
-        np.testing.assert_array_equal(ar.view(it[4]).cpu().numpy(), batched[i])
+        assert rel_err(ar.view(it[4]).cpu().numpy(), batched[i]) <= 1e-12
     ar.close()
