@@ -86,8 +86,10 @@ struct GraphEntry {
 struct bri_ctx {
   int device = 0;
   cudaStream_t side = nullptr;    // lookahead: bulk trailing updates of the LU
+  cudaStream_t side2 = nullptr;   // folded right-hand side of the Schur LU (LuFold)
   cudaStream_t gstream = nullptr; // graphs are captured / launched here
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_x = nullptr, ev_in = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_x = nullptr, ev_d = nullptr, ev_w = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::vector<GraphEntry> graphs; // captured hot-path sequences (LRU, <= 16)
   std::vector<std::vector<uintptr_t>> seen;
   DevBuf items;   // uploaded item arrays
@@ -199,8 +201,30 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
 //     side stream updates everything else.
 //   Either way the pivot chain (panels) overlaps the bulk trailing GEMMs.
 // dev_slots: F slots; dev_ffff: (F, F, F, F) quads; dev_ff: (F, F) pairs.
+//
+// fold: a forward sweep rides along as extra columns of the factorization,
+// on a second side stream that trails the panels, so only the U sweep is
+// left after the factorization.  The left-of-block interchanges of L are
+// skipped then (nothing reads the final L).
+//   * Schur nodes: W = L^-1 P l — W <- l, then per outer block J its
+//     interchanges, the L11 solve of J's rows and the rank-128 update of the
+//     rows below;
+//   * explicit inverses (tri): W = L^-1 itself — W <- I; per block J the
+//     interchanges of W's columns [0, J0) (the rows of the L computed so
+//     far: keeps W the inverse of the current L), then the solve and update
+//     restricted to columns [0, J0 + 128) (W stays unit lower triangular),
+//     n^3 / 3 flops in all.
+struct LuFold {
+  const int* w;      // W slots
+  const int* lw;     // (l, W) copy pairs (unused when tri)
+  const int* fw;     // (F, W) pairs (triangular solve)
+  const int* fwww;   // (F, W, W, W) quads (update GEMM)
+  cudaEvent_t ev_l;  // external event gating l (nullptr: resident)
+  bool tri;          // W = L^-1 (explicit inverse) instead of L^-1 P l
+};
+
 int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, const int* dev_ff,
-                 int count, const LuLayout& L, const LuScratch& sc) {
+                 int count, const LuLayout& L, const LuScratch& sc, const LuFold* fold = nullptr) {
   const ArenaView& v = ar->v;
   const int n = v.n;
   bri_ctx* ctx = ar->ctx;
@@ -253,6 +277,42 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   }();
   const int trail_cap = trail_cap_env >= 0 ? trail_cap_env : (count <= 2 ? 80 : 0);
 
+  static const int fold_cap_env = [] {
+    const char* e = getenv("BRI_FOLD_CAP");
+    return e ? atoi(e) : -1;
+  }();
+  const int fold_cap = fold_cap_env >= 0 ? fold_cap_env : (count <= 2 ? 48 : 0);
+  // W <- L11^-1 P_J W on block J's rows, then W[N0:, :] -= L21 W[J rows, :]
+  auto fold_block = [&](cudaStream_t st, int J0, int W, int pidx0, int npan) -> int {
+    const bool tri = fold->tri;
+    const int ncol = tri ? J0 + W : n;
+    if (J0 == 0) {
+      if (tri) {
+        BRI_CHECK(launch_identity(v, fold->w, 1, count, st));
+      } else {
+        if (fold->ev_l) BRI_CHECK(cudaStreamWaitEvent(st, fold->ev_l, cudaEventWaitExternal));
+        BRI_CHECK(launch_copy(v, fold->lw, count, st));
+      }
+    }
+    BRI_CHECK(launch_laswp(v, fold->w, count, J0, W, nbi, pidx0, npan, 0, tri ? J0 : n, 0, 0, sc, n,
+                           L.pair_stride, st));
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, v, fold->fw, count, dl, true, J0, W, 0, ncol, tri, st));
+    if (n - J0 - W > 0)
+      return gemm_call(ar, st, fold->fwww, count, n - J0 - W, ncol, W, J0 + W, J0, J0, 0, J0 + W, 0, -1.0, 1.0,
+                       fold_cap);
+    return 0;
+  };
+  // hand block J (factored, its L11 inverse in dl, both ordered before `ev`
+  // on `from`) to the fold stream
+  cudaStream_t s2 = ctx->side2;
+  auto fold_after = [&](cudaStream_t from, int J0, int W, int pidx0, int npan) -> int {
+    if (!fold) return 0;
+    BRI_CHECK(cudaEventRecord(ctx->ev_d, from));
+    BRI_CHECK(cudaStreamWaitEvent(s2, ctx->ev_d, 0));
+    return fold_block(s2, J0, W, pidx0, npan);
+  };
+  const int left = fold ? 0 : 1;   // 0: skip the interchanges of L left of the block
+
   const int npan_outer = outer / nbi;
   static const bool lookahead = [] {
     const char* e = getenv("BRI_LOOKAHEAD");
@@ -279,9 +339,11 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     const int WNN = (n - N1) < outer ? (n - N1) : outer;
     if ((J0 % TRSM_BLOCK) != 0) return fail_msg("getrf: outer block not aligned to the TRSM block");
     if (WN > 0 && !lookahead) {
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N0, n, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N0, n, sc, n,
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
+      if (fold)
+        if (int rc = fold_block(s, J0, W, pidx0, npan)) return rc;
       if (int rc = update_cols(s, J0, W, pidx0, N0, n, 0)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
     } else if (WN > 0 && !extend) {
@@ -290,10 +352,11 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
                              L.pair_stride, s));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
       BRI_CHECK(cudaEventRecord(ctx->ev_a, s));
+      if (int rc = fold_after(s, J0, W, pidx0, npan)) return rc;
       if (int rc = update_cols(s, J0, W, pidx0, N0, N1, 0)) return rc;
       // bulk: everything else, concurrently on the side stream
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N1, n, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1, n, sc, n,
                              L.pair_stride, s1));
       if (int rc = update_cols(s1, J0, W, pidx0, N1, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
@@ -304,22 +367,35 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       BRI_CHECK(cudaEventRecord(ctx->ev_a, s));
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
       BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s1));
+      if (int rc = fold_after(s1, J0, W, pidx0, npan)) return rc;
       if (WNN > 0) {   // block J+2's columns first: block J+1's inner panels extend into them
         BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, N1, N1 + WNN, 0, 0, sc, n,
                                L.pair_stride, s1));
         if (int rc = update_cols(s1, J0, W, pidx0, N1, N1 + WNN, 0)) return rc;
         BRI_CHECK(cudaEventRecord(ctx->ev_x, s1));
       }
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, N1 + WNN, n, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1 + WNN, n, sc, n,
                              L.pair_stride, s1));
       if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1 + WNN, WNN > 0 ? ctx->ev_x : nullptr)) return rc;
       BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     } else {
-      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0, 0, 0, sc, n,
+      BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, 0, 0, sc, n,
                              L.pair_stride, s));
+      if (fold) {   // last block: its L11 inverse, then W's last rows
+        BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
+        if (lookahead) {
+          if (int rc = fold_after(s, J0, W, pidx0, npan)) return rc;
+        } else if (int rc = fold_block(s, J0, W, pidx0, npan)) {
+          return rc;
+        }
+      }
     }
+  }
+  if (fold && lookahead) {
+    BRI_CHECK(cudaEventRecord(ctx->ev_w, s2));
+    BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_w, 0));
   }
   BRI_CHECK(launch_diag_check(v, dev_slots, count, sc.scale_bits, sc.status, s));
   return 0;
@@ -336,14 +412,14 @@ int ensure_dinv(bri_arena* ar, cudaStream_t s, int count) {
 // just computed by getrf_device on this stream, which already inverted every
 // L diagonal block but those of its last outer block.
 int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, double** dl, double** du,
-              bool after_getrf = false) {
+              bool after_getrf = false, bool want_l = true) {
   const int n = ar->v.n;
   const size_t per = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
   if (int rc = ar->ctx->dinv.ensure(2 * per * count * sizeof(double), s)) return rc;
   *dl = static_cast<double*>(ar->ctx->dinv.ptr);
   *du = *dl + per * count;
   const int l0 = after_getrf ? ((n - 1) / LU_OUTER) * LU_OUTER / TRSM_BLOCK : 0;
-  BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, l0, 0, s));
+  if (want_l) BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, true, *dl, l0, 0, s));
   BRI_CHECK(launch_dinv(ar->v, dev_fslots, count, false, *du, 0, 0, s));
   return 0;
 }
@@ -566,6 +642,9 @@ int bri_ctx_create(int device, bri_ctx** out) {
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+  BRI_CHECK(cudaEventCreateWithFlags(&c->ev_d, cudaEventDisableTiming));
+  BRI_CHECK(cudaEventCreateWithFlags(&c->ev_w, cudaEventDisableTiming));
+  BRI_CHECK(cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_low));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
   BRI_CHECK(cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, prio_high));
@@ -587,6 +666,9 @@ void bri_ctx_destroy(bri_ctx* ctx) {
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
+  if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
+  if (ctx->ev_w) cudaEventDestroy(ctx->ev_w);
+  if (ctx->side2) cudaStreamDestroy(ctx->side2);
   delete ctx;
 }
 
@@ -744,9 +826,9 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
     BRI_CHECK(launch_small_node(ar->v, dev, count, 1, status, s));
     return 0;
   }
-  // layout: [F slots | (in,F) pairs | (F,F,F,F) | (F,out) | (F,out,out,out)]
+  // layout: [F slots | (in,F) pairs | (F,F,F,F) | (F,out) | (F,out,out,out) | (F,F) | (out,F) | out]
   std::vector<int> h;
-  h.reserve(13 * (size_t)count);
+  h.reserve(18 * (size_t)count);
   for (int i = 0; i < count; ++i) h.push_back(items[3 * i + 1]);
   for (int i = 0; i < count; ++i) { h.push_back(items[3 * i]); h.push_back(items[3 * i + 1]); }
   for (int i = 0; i < count; ++i) for (int q = 0; q < 4; ++q) h.push_back(items[3 * i + 1]);
@@ -757,6 +839,7 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
   }
   for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 1]); h.push_back(items[3 * i + 1]); }
   for (int i = 0; i < count; ++i) { h.push_back(items[3 * i + 2]); h.push_back(items[3 * i + 1]); }
+  for (int i = 0; i < count; ++i) h.push_back(items[3 * i + 2]);
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int* d_ff = dev + 13 * count;
@@ -770,8 +853,23 @@ int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, i
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
   if (int rc = ensure_dinv(ar, s, count)) return rc;
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  static const int fold_env = [] {
+    const char* e = getenv("BRI_FOLD");
+    return e ? atoi(e) : -1;
+  }();
+  const bool fold_on = fold_env >= 0 ? fold_env != 0 : count <= 2;
   auto issue = [&](cudaStream_t st) -> int {
     BRI_CHECK(launch_copy(ar->v, d_inf, count, st));
+    if (fold_on) {   // T = L^-1 built during the factorization, then the U sweep
+      const LuFold fold{dev + 17 * count, nullptr, d_fo, d_fooo, nullptr, true};
+      if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, count, L, sc, &fold)) return rc;
+      double *dl = nullptr, *du = nullptr;
+      if (int rc = make_dinv(ar, st, d_f, count, &dl, &du, true, false)) return rc;
+      if (int rc = trsm_rec(ar, st, d_fo, d_fooo, count, false, 0, n, n, du)) return rc;
+      BRI_CHECK(launch_colscatter(ar->v, d_of, count, sc.pi, n, st));
+      BRI_CHECK(launch_copy(ar->v, d_fo, count, st));
+      return 0;
+    }
     if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, count, L, sc)) return rc;
     // X^-1 = U^-1 L^-1 P (dgetri order): T = U^-1 (L^-1 I) with the L sweep
     // exploiting the triangular identity (n^3/3 instead of n^3), then the
@@ -813,9 +911,9 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
     BRI_CHECK(launch_small_node(ar->v, dev, count, 0, status, s));
     return 0;
   }
-  // layout: [F | (p,F) | (F,F,F,F) | (l,W) | (F,W) | (F,W,W,W) | (rt,W,r,out)]
+  // layout: [F | (p,F) | (F,F,F,F) | (l,W) | (F,W) | (F,W,W,W) | (rt,W,r,out) | (F,F) | W]
   std::vector<int> h;
-  h.reserve(17 * (size_t)count);
+  h.reserve(22 * (size_t)count);
   for (int i = 0; i < count; ++i) h.push_back(I(i, 5));
   for (int i = 0; i < count; ++i) { h.push_back(I(i, 0)); h.push_back(I(i, 5)); }
   for (int i = 0; i < count; ++i) for (int q = 0; q < 4; ++q) h.push_back(I(i, 5));
@@ -832,6 +930,7 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
     h.push_back(I(i, 4));
   }
   for (int i = 0; i < count; ++i) { h.push_back(I(i, 5)); h.push_back(I(i, 5)); }
+  for (int i = 0; i < count; ++i) h.push_back(I(i, 6));
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int* d_f = dev;
@@ -845,13 +944,30 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
   if (int rc = ensure_dinv(ar, s, count)) return rc;
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  // the fold pays when the panel chain leaves SMs idle (batches of <= 2:
+  // config 2 31.4 -> 30.1 ms/step); large batches are throughput-bound and
+  // its rank-128 updates are slower than the recursive sweep (config 3
+  // 1.52 -> 1.64 s)
+  static const int fold_env = [] {
+    const char* e = getenv("BRI_FOLD");
+    return e ? atoi(e) : -1;
+  }();
+  const bool fold_on = fold_env >= 0 ? fold_env != 0 : count <= 2;
   auto issue = [&](cudaStream_t s) -> int {
   BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
-  if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc)) return rc;
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
-  if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
-  BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
-  if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count, false, true)) return rc;
+  if (fold_on) {
+    const LuFold fold{dev + 21 * count, d_lw, d_fw, d_fwww, static_cast<cudaEvent_t>(ev_l), false};
+    if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc, &fold)) return rc;
+    double *dl = nullptr, *du = nullptr;
+    if (int rc = make_dinv(ar, s, d_f, count, &dl, &du, true, false)) return rc;
+    if (int rc = trsm_rec(ar, s, d_fw, d_fwww, count, false, 0, n, n, du)) return rc;
+  } else {
+    if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc)) return rc;
+    if (ev_l) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
+    BRI_CHECK(launch_permcopy(ar->v, d_lw, count, sc.pi, n, false, s));
+    if (int rc = getrs_sweeps(ar, s, d_f, d_fw, d_fwww, count, false, true)) return rc;
+  }
   if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
   return gemm_call(ar, s, d_final, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
   };

@@ -399,10 +399,12 @@ def test_tall_block_node_matches_oracle(bri):
     assert rel_err(got, ref) <= 1e-9
 
 
-@pytest.mark.parametrize("env", [{"BRI_LOOKAHEAD": "0"}, {"BRI_LU_EXTEND": "0"}, {"BRI_LU_EXTEND": "1"}])
+@pytest.mark.parametrize("env", [{"BRI_LOOKAHEAD": "0"}, {"BRI_LU_EXTEND": "0"}, {"BRI_LU_EXTEND": "1"},
+                                 {"BRI_FOLD": "0"}, {"BRI_FOLD": "1"}, {"BRI_LOOKAHEAD": "0", "BRI_FOLD": "1"}])
 def test_lu_schedules_agree(bri, env, tmp_path):
-    """The three LU schedules (no lookahead; lookahead; lookahead with inner panels
-    extended into the next outer block, the default for batches of <= 2) each give the
+    """The LU schedules (no lookahead; lookahead; lookahead with inner panels extended
+    into the next outer block; with or without the forward sweep folded into the
+    factorization — extension and fold are the defaults for batches of <= 2) each give the
     dense inverse and the BRI blocks as accurately as the default schedule (errors against
     numpy's LAPACK inverse; the BRI pivot blocks are poorly conditioned on purpose, so
     schedules that round differently differ by far more than 1 ulp there)."""
