@@ -108,6 +108,10 @@ cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
 int trsm_smem_bytes();
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
                         int blk0, int nblocks, cudaStream_t s);
+// X * U[J0:J0+W, J0:J0+W] = B in place on columns [J0, J0 + W) of G, all rows;
+// gf: device (G, F) pairs; dinv_u: inverted upper diagonal blocks of F
+cudaError_t launch_rtrsm(const ArenaView& a, const int* gf, int count, const double* dinv_u, int J0, int W,
+                         cudaStream_t s);
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const CUtensorMap& tmB16,
                               const ArenaView& a, const int* fw, int count, const double* dinv, bool lower, int r0,
                               int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s);

@@ -221,6 +221,14 @@ struct LuFold {
   const int* fwww;   // (F, W, W, W) quads (update GEMM)
   cudaEvent_t ev_l;  // external event gating l (nullptr: resident)
   bool tri;          // W = L^-1 (explicit inverse) instead of L^-1 P l
+  // Schur nodes, optional: C = rt U^-1 in slot G as well — G <- rt, then per
+  // outer block J (once U's block row J is final) C_J = G_J U_JJ^-1 (right
+  // solve) and G[:, J0 + 128:] -= C_J U[J, J0 + 128:].  Leaves only
+  // out = r - C W after the factorization.
+  const int* gf = nullptr;     // (G, F) pairs (nullptr: no C fold)
+  const int* gfgg = nullptr;   // (G, F, G, G) quads
+  const int* rtg = nullptr;    // (rt, G) copy pairs
+  cudaEvent_t ev_rtr = nullptr;
 };
 
 int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, const int* dev_ff,
@@ -302,6 +310,26 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
                        fold_cap);
     return 0;
   };
+  double* du = dl + per * count;
+  auto fold_c = [&](cudaStream_t st, int J0, int W) -> int {
+    if (!fold || !fold->gf) return 0;
+    if (J0 == 0) {
+      if (fold->ev_rtr) BRI_CHECK(cudaStreamWaitEvent(st, fold->ev_rtr, cudaEventWaitExternal));
+      BRI_CHECK(launch_copy(v, fold->rtg, count, st));
+    }
+    BRI_CHECK(launch_dinv(v, dev_slots, count, false, du, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, st));
+    BRI_CHECK(launch_rtrsm(v, fold->gf, count, du, J0, W, st));
+    if (n - J0 - W > 0)
+      return gemm_call(ar, st, fold->gfgg, count, n, n - J0 - W, W, 0, J0, J0, J0 + W, 0, J0 + W, -1.0, 1.0,
+                       fold_cap);
+    return 0;
+  };
+  // C part of block J once its U row block is final (recorded as ev_b on s1)
+  auto fold_c_after_b = [&](int J0, int W) -> int {
+    if (!fold || !fold->gf) return 0;
+    BRI_CHECK(cudaStreamWaitEvent(ctx->side2, ctx->ev_b, 0));
+    return fold_c(ctx->side2, J0, W);
+  };
   // hand block J (factored, its L11 inverse in dl, both ordered before `ev`
   // on `from`) to the fold stream
   cudaStream_t s2 = ctx->side2;
@@ -345,6 +373,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       if (fold)
         if (int rc = fold_block(s, J0, W, pidx0, npan)) return rc;
       if (int rc = update_cols(s, J0, W, pidx0, N0, n, 0)) return rc;
+      if (int rc = fold_c(s, J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
     } else if (WN > 0 && !extend) {
       // critical path: next block's columns, then factor it
@@ -360,6 +389,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
                              L.pair_stride, s1));
       if (int rc = update_cols(s1, J0, W, pidx0, N1, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
+      if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
       BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     } else if (WN > 0) {
@@ -378,6 +408,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
                              L.pair_stride, s1));
       if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, trail_cap)) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
+      if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1 + WNN, WNN > 0 ? ctx->ev_x : nullptr)) return rc;
       BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_b, 0));
     } else {
@@ -387,8 +418,10 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
         BRI_CHECK(launch_dinv(v, dev_slots, count, true, dl, J0 / TRSM_BLOCK, (W + TRSM_BLOCK - 1) / TRSM_BLOCK, s));
         if (lookahead) {
           if (int rc = fold_after(s, J0, W, pidx0, npan)) return rc;
-        } else if (int rc = fold_block(s, J0, W, pidx0, npan)) {
-          return rc;
+          if (int rc = fold_c(s2, J0, W)) return rc;
+        } else {
+          if (int rc = fold_block(s, J0, W, pidx0, npan)) return rc;
+          if (int rc = fold_c(s, J0, W)) return rc;
         }
       }
     }
@@ -911,9 +944,10 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
     BRI_CHECK(launch_small_node(ar->v, dev, count, 0, status, s));
     return 0;
   }
-  // layout: [F | (p,F) | (F,F,F,F) | (l,W) | (F,W) | (F,W,W,W) | (rt,W,r,out) | (F,F) | W]
+  // layout: [F | (p,F) | (F,F,F,F) | (l,W) | (F,W) | (F,W,W,W) | (rt,W,r,out) | (F,F) | W |
+  //          (out,F) | (out,F,out,out) | (rt,out) | (out,W,r,F) | (F,out)]   (G = out in the C fold)
   std::vector<int> h;
-  h.reserve(22 * (size_t)count);
+  h.reserve(36 * (size_t)count);
   for (int i = 0; i < count; ++i) h.push_back(I(i, 5));
   for (int i = 0; i < count; ++i) { h.push_back(I(i, 0)); h.push_back(I(i, 5)); }
   for (int i = 0; i < count; ++i) for (int q = 0; q < 4; ++q) h.push_back(I(i, 5));
@@ -931,6 +965,21 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
   }
   for (int i = 0; i < count; ++i) { h.push_back(I(i, 5)); h.push_back(I(i, 5)); }
   for (int i = 0; i < count; ++i) h.push_back(I(i, 6));
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 4)); h.push_back(I(i, 5)); }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(I(i, 4));
+    h.push_back(I(i, 5));
+    h.push_back(I(i, 4));
+    h.push_back(I(i, 4));
+  }
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 1)); h.push_back(I(i, 4)); }
+  for (int i = 0; i < count; ++i) {
+    h.push_back(I(i, 4));
+    h.push_back(I(i, 6));
+    h.push_back(I(i, 3));
+    h.push_back(I(i, 5));
+  }
+  for (int i = 0; i < count; ++i) { h.push_back(I(i, 5)); h.push_back(I(i, 4)); }
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int* d_f = dev;
@@ -953,9 +1002,31 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
     return e ? atoi(e) : -1;
   }();
   const bool fold_on = fold_env >= 0 ? fold_env != 0 : count <= 2;
+  // opt-in: folding C = rt U^-1 as well moves the U sweep into the
+  // factorization, but the side streams cannot absorb its 2 n^3 flops next to
+  // the panel chain (config 2: 28.5 -> 30.9 ms/step at the best caps, the
+  // fold stream ends 4 ms after the last panel)
+  static const bool fold_c_on = [] {
+    const char* e = getenv("BRI_FOLD_C");
+    return e != nullptr && e[0] == '1';
+  }();
   auto issue = [&](cudaStream_t s) -> int {
   BRI_CHECK(launch_copy(ar->v, d_pf, count, s));
   // W = P^-1 l  (X-world: W = (p^)^-1 l^ via dgetrs), then out = r - rt * W
+  if (fold_on && fold_c_on) {
+    // both sweeps folded: W = L^-1 P l and C = rt U^-1 (in `out`) come out of
+    // the factorization; F = r - C W, then out <- F
+    LuFold fold{dev + 21 * count, d_lw, d_fw, d_fwww, static_cast<cudaEvent_t>(ev_l), false};
+    fold.gf = dev + 22 * count;
+    fold.gfgg = dev + 24 * count;
+    fold.rtg = dev + 28 * count;
+    fold.ev_rtr = static_cast<cudaEvent_t>(ev_rtr);
+    if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc, &fold)) return rc;
+    if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
+    if (int rc = gemm_call(ar, s, dev + 30 * count, count, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0)) return rc;
+    BRI_CHECK(launch_copy(ar->v, dev + 34 * count, count, s));
+    return 0;
+  }
   if (fold_on) {
     const LuFold fold{dev + 21 * count, d_lw, d_fw, d_fwww, static_cast<cudaEvent_t>(ev_l), false};
     if (int rc = getrf_device(ar, s, d_f, d_ffff, dev + 19 * count, count, L, sc, &fold)) return rc;

@@ -267,6 +267,107 @@ __global__ void __launch_bounds__(THREADS, 2)
   }
 }
 
+
+// --------------------------------------------------------------- right solve
+// X * U[J, J] = B in place on columns [J0, J0 + W) of slot G (all n rows),
+// U from the factor in slot F with its inverted 64 x 64 diagonal blocks in
+// `dinv` (dinv_kernel<false>): per 64-column block b,
+//     X_b = (B_b - sum_{a < b} X_a U_ab) * Uinv_bb.
+// Rows are independent, so one CTA owns RT_R rows and the whole block: the
+// in-place update needs no cross-CTA ordering.  Used by the folded Schur
+// update (capi.cu getrf_device): C = rt * U^-1, 128 columns per outer block.
+constexpr int RT_R = 32;               // rows per CTA
+constexpr int RT_THREADS = 128;        // 4 warps: 2 along M (16 rows) x 2 along N (32 cols)
+constexpr int RT_LDX = RT_R + 8;       // [col][row] tiles (A-operand pattern)
+constexpr int RT_LDU = T + 4;          // [n][k] tiles (B-operand pattern)
+constexpr int RT_SMEM = (3 * T * RT_LDX + T * RT_LDU) * 8;
+
+struct RtrsmArgs {
+  double* base;
+  int ld, n;
+  long long slot_elems;
+  const int* items;      // (G, F) per item
+  const double* dinv;    // per item [nblk][T*T], upper
+  int nblk, J0, W;
+};
+
+__global__ void __launch_bounds__(RT_THREADS) rtrsm_kernel(RtrsmArgs p) {
+  extern __shared__ double rt_smem[];
+  double* Xs = rt_smem;                       // X_0, X_1: [col][row]
+  double* As = Xs + 2 * T * RT_LDX;           // B_b - ..., [col][row]
+  double* Us = As + T * RT_LDX;               // U_ab or Uinv_bb, [n][k]
+  const int item = blockIdx.y, m0 = blockIdx.x * RT_R;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp & 1) * 16, wn0 = (warp >> 1) * 32;
+  double* G = p.base + (long long)p.items[2 * item] * p.slot_elems;
+  const double* F = p.base + (long long)p.items[2 * item + 1] * p.slot_elems;
+  const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
+  const int nbw = (p.W + T - 1) / T;
+  for (int b = 0; b < nbw; ++b) {
+    const int cb = p.J0 + b * T, wb = min(T, p.W - b * T);
+    for (int e = tid; e < T * RT_R; e += RT_THREADS) {
+      const int r = e % RT_R, cc = e / RT_R;
+      As[cc * RT_LDX + r] = (m0 + r < p.n && cc < wb) ? G[(m0 + r) + (long long)(cb + cc) * p.ld] : 0.0;
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        acc[j][v] = As[(wn0 + j * 8 + 2 * t + (v & 1)) * RT_LDX + wm0 + g + ((v >> 1) << 3)];
+    for (int a = 0; a < b; ++a) {
+      const int ra = p.J0 + a * T;
+      for (int e = tid; e < T * T; e += RT_THREADS) {
+        const int k = e % T, nn = e / T;
+        Us[nn * RT_LDU + k] = nn < wb ? F[(ra + k) + (long long)(cb + nn) * p.ld] : 0.0;
+      }
+      __syncthreads();
+      const double* Xa = Xs + a * T * RT_LDX;
+#pragma unroll 4
+      for (int k0 = 0; k0 < T; k0 += 4) {
+        const double a0 = -Xa[(k0 + t) * RT_LDX + wm0 + g], a1 = -Xa[(k0 + t) * RT_LDX + wm0 + g + 8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[j], a0, a1, Us[(wn0 + j * 8 + g) * RT_LDU + k0 + t]);
+      }
+      __syncthreads();
+    }
+    const double* Di = dinv + (long long)(cb / T) * T * T;
+    for (int e = tid; e < T * T; e += RT_THREADS) {
+      const int k = e % T, nn = e / T;
+      Us[nn * RT_LDU + k] = Di[nn * T + k];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        As[(wn0 + j * 8 + 2 * t + (v & 1)) * RT_LDX + wm0 + g + ((v >> 1) << 3)] = acc[j][v];
+    __syncthreads();
+    double x[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) x[j][v] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < T; k0 += 4) {
+      const double a0 = As[(k0 + t) * RT_LDX + wm0 + g], a1 = As[(k0 + t) * RT_LDX + wm0 + g + 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_16x8x4(x[j], a0, a1, Us[(wn0 + j * 8 + g) * RT_LDU + k0 + t]);
+    }
+    double* Xb = Xs + b * T * RT_LDX;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        Xb[(wn0 + j * 8 + 2 * t + (v & 1)) * RT_LDX + wm0 + g + ((v >> 1) << 3)] = x[j][v];
+    __syncthreads();
+    for (int e = tid; e < T * RT_R; e += RT_THREADS) {
+      const int r = e % RT_R, cc = e / RT_R;
+      if (m0 + r < p.n && cc < wb) G[(m0 + r) + (long long)(cb + cc) * p.ld] = Xb[cc * RT_LDX + r];
+    }
+    // the next block's loads overwrite As / Us only after the barrier at its top
+  }
+}
 }  // namespace
 
 int trsm_smem_bytes() { return smem_bytes<32, 3>(); }
@@ -280,7 +381,25 @@ cudaError_t configure_trsm() {
   set((const void*)trsm_kernel<false, 32, 3>, smem_bytes<32, 3>());
   set((const void*)trsm_kernel<true, 16, 4>, smem_bytes<16, 4>());
   set((const void*)trsm_kernel<false, 16, 4>, smem_bytes<16, 4>());
+  set((const void*)rtrsm_kernel, RT_SMEM);
   return e;
+}
+
+cudaError_t launch_rtrsm(const ArenaView& a, const int* gf, int count, const double* dinv_u, int J0, int W,
+                         cudaStream_t s) {
+  RtrsmArgs p;
+  p.base = a.base;
+  p.ld = a.ld;
+  p.n = a.n;
+  p.slot_elems = a.slot_elems;
+  p.items = gf;
+  p.dinv = dinv_u;
+  p.nblk = (a.n + T - 1) / T;
+  p.J0 = J0;
+  p.W = W;
+  count_launch();
+  rtrsm_kernel<<<dim3((a.n + RT_R - 1) / RT_R, count), RT_THREADS, RT_SMEM, s>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,

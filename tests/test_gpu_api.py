@@ -400,7 +400,8 @@ def test_tall_block_node_matches_oracle(bri):
 
 
 @pytest.mark.parametrize("env", [{"BRI_LOOKAHEAD": "0"}, {"BRI_LU_EXTEND": "0"}, {"BRI_LU_EXTEND": "1"},
-                                 {"BRI_FOLD": "0"}, {"BRI_FOLD": "1"}, {"BRI_LOOKAHEAD": "0", "BRI_FOLD": "1"}])
+                                 {"BRI_FOLD": "0"}, {"BRI_FOLD": "1"}, {"BRI_LOOKAHEAD": "0", "BRI_FOLD": "1"},
+                                 {"BRI_FOLD": "1", "BRI_FOLD_C": "1"}, {"BRI_FOLD_C": "1"}])
 def test_lu_schedules_agree(bri, env, tmp_path):
     """The LU schedules (no lookahead; lookahead; lookahead with inner panels extended
     into the next outer block; with or without the forward sweep folded into the
