@@ -294,7 +294,10 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
           bulk_s2cluster(dsmem_addr(&cmsg[par][rank], lane), out, sizeof(CandMsg), dsmem_addr(&xbar[par], lane));
       }
       PPROF(1);
-      mbar_wait_cluster(&xbar[par], (jj >> 1) & 1);
+      // CTA-scope acquire: the messages land in this CTA's shared memory
+      // through the bulk copies' complete_tx, which orders them; an
+      // acquire.cluster here costs a CCTL.IVALL (L1 flush) per column
+      mbar_wait(&xbar[par], (jj >> 1) & 1);
       PPROF(2);
       // ---- (3) global winner
       double gv = lane < cs ? cmsg[par][lane].val : -1.0;
