@@ -49,10 +49,22 @@ def free_bytes(device: int) -> int:
     torch = _torch()
     if device not in _FREE0:
         free, _ = torch.cuda.mem_get_info(device)
-        _FREE0[device] = (free, torch.cuda.memory_reserved(device))
+        _FREE0[device] = (free, _torch_bytes(device)[0])
     free0, res0 = _FREE0[device]
-    reserved = torch.cuda.memory_reserved(device)
-    return max(0, free0 - (reserved - res0)) + (reserved - torch.cuda.memory_allocated(device))
+    reserved, allocated = _torch_bytes(device)
+    return max(0, free0 - (reserved - res0)) + (reserved - allocated)
+
+
+def _torch_bytes(device: int):
+    """(reserved, allocated) bytes of PyTorch's caching allocator.  Reads the raw
+    nested statistics: torch.cuda.memory_reserved() flattens all of them first
+    (~0.2 ms per call, on every run's critical host path)."""
+    torch = _torch()
+    try:
+        st = torch._C._cuda_memoryStats(device)
+        return int(st["reserved_bytes"]["all"]["current"]), int(st["allocated_bytes"]["all"]["current"])
+    except (AttributeError, KeyError, TypeError):
+        return torch.cuda.memory_reserved(device), torch.cuda.memory_allocated(device)
 
 
 def padded_ld(n: int) -> int:

@@ -249,8 +249,10 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
     nslots = min(max_slots, base_need + 2 * chunk + 1)
     info = RunInfo("dag", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),
                    {n: len(v) for n, v in levels.items()}, nslots, chunk)
-    status = torch.zeros(max(1, len(sched.nodes)), dtype=torch.int32, device=f"cuda:{device}")
-    root_status = torch.zeros(max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
+    # one status tensor (nodes, then roots): one fill, one device -> host read
+    nst = max(1, len(sched.nodes))
+    st_all = torch.zeros(nst + max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
+    status, root_status = st_all[:nst], st_all[nst:]
     results = []
     arena = cached_arena(b, nslots, device, gauge=ws.gauge)
     try:
@@ -330,8 +332,9 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
         else:
             for t in range(nroots):
                 results.append(arena.view(val[sched.roots[t]]).clone())
-        node_status = status[: len(sched.nodes)].cpu().numpy()  # synchronizes the stream
-        rstat = root_status[:nroots].cpu().numpy() if invert_roots else None
+        st_host = st_all.cpu().numpy()  # synchronizes the stream
+        node_status = st_host[: len(sched.nodes)]
+        rstat = st_host[nst:nst + nroots] if invert_roots else None
         # map device positions back to node ids
         pstat = np.zeros(len(sched.nodes), dtype=np.int64)
         for nid, p in pos.items():

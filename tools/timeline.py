@@ -35,7 +35,7 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     torch.cuda.synchronize()
 path = "/tmp/bri_trace.json"
 prof.export_chrome_trace(path)
-ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
+ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") in ("kernel", "gpu_memcpy")]
 ev.sort(key=lambda e: e["ts"])
 
 
