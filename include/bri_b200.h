@@ -148,6 +148,23 @@ int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, dou
                   long long ldo);
 
 /*
+ * Seeded Gaussian test matrix M = G + shift * I of order m, generated blockwise
+ * on the device (BASELINE config 5: "M = G + m I, G i.i.d. N(0,1) generated
+ * blockwise from seed 4"; the reference has no blockwise scheme, it draws the
+ * whole matrix from one PCG64 stream, cli.py:122-130).  Element (r, c) takes
+ * Philox4x64-10 (numpy's np.random.Philox) at counter ((r*m + c) / 4, 0, 0, 0)
+ * with key (seed, 0), then Box-Muller on the output pair (r*m + c) % 4 / 2
+ * (cos for even, sin for odd r*m + c).  Indices >= m are identity padding.
+ * bri_randn_blocks writes view blocks (i, j) of order n_arena into slots
+ * (items as bri_rbf_blocks, optional rmap/cmap); bri_randn_window writes the
+ * rows x cols window at (row0, col0) row-major into out (leading dim ldo).
+ */
+int bri_randn_blocks(bri_arena* arena, void* stream, long long m, unsigned long long seed, double shift,
+                     const int* rmap, const int* cmap, int count, const int* items);
+int bri_randn_window(void* stream, long long m, unsigned long long seed, double shift, long long row0,
+                     long long col0, int rows, int cols, double* out, long long ldo);
+
+/*
  * Host -> device block loads — the fetch of providers.py:318-336 for a matrix in
  * (pinned) host memory: one 2-D async copy per item (block row i, block col j,
  * slot), 0-based, from the row-major host matrix with leading dim ldh into the

@@ -301,3 +301,64 @@ def kernel_matrix(inputs: np.ndarray, gamma: float = 1.0, sigma: float = 1.0) ->
 def predicted_nodes(k: int) -> int:
     """(4^(k-1) - 1) / 3 Schur nodes per target (instrumentation.py:124-139)."""
     return (4 ** (k - 1) - 1) // 3
+
+
+# --------------------------------------------------------------------------
+# Config-5 input: seeded Gaussian matrix generated blockwise (no reference
+# counterpart: the reference draws M from one PCG64 stream, cli.py:122-130,
+# which cannot produce a block without the blocks before it).  Restated here
+# from Random123's Philox4x64-10 — the algorithm behind numpy's
+# np.random.Philox, against which tests/test_oracle.py pins it — plus the
+# Box-Muller map documented in include/bri_b200.h (bri_randn_blocks).
+# --------------------------------------------------------------------------
+
+_PH_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+_PH_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+_MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def _mul_hilo(a: int, x: np.ndarray):
+    """(hi, lo) 64-bit halves of the 128-bit products a * x (x uint64 array)."""
+    a_lo, a_hi = np.uint64(a & 0xFFFFFFFF), np.uint64(a >> 32)
+    x_lo, x_hi = x & _MASK32, x >> np.uint64(32)
+    ll, lh = a_lo * x_lo, a_lo * x_hi
+    hl, hh = a_hi * x_lo, a_hi * x_hi
+    mid = (ll >> np.uint64(32)) + (lh & _MASK32) + (hl & _MASK32)
+    hi = hh + (lh >> np.uint64(32)) + (hl >> np.uint64(32)) + (mid >> np.uint64(32))
+    lo = (mid << np.uint64(32)) | (ll & _MASK32)
+    return hi, lo
+
+
+def philox4x64_10(counter0: np.ndarray, key0: int, key1: int = 0) -> np.ndarray:
+    """Philox4x64-10 outputs (n, 4) uint64 for counters (counter0[i], 0, 0, 0)."""
+    c = [np.asarray(counter0, dtype=np.uint64).copy()] + [np.zeros(np.shape(counter0), np.uint64)] * 3
+    k0, k1 = key0 & 0xFFFFFFFFFFFFFFFF, key1 & 0xFFFFFFFFFFFFFFFF
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            hi0, lo0 = _mul_hilo(_PH_M[0], c[0])
+            hi1, lo1 = _mul_hilo(_PH_M[1], c[2])
+            c = [hi1 ^ c[1] ^ np.uint64(k0), lo1, hi0 ^ c[3] ^ np.uint64(k1), lo0]
+            k0 = (k0 + _PH_W[0]) & 0xFFFFFFFFFFFFFFFF
+            k1 = (k1 + _PH_W[1]) & 0xFFFFFFFFFFFFFFFF
+    return np.stack(c, axis=-1)
+
+
+def gaussian_window(m: int, seed: int, shift: float, row0: int, col0: int, rows: int, cols: int) -> np.ndarray:
+    """Window [row0:row0+rows, col0:col0+cols] of M = G + shift*I (order m, identity padding beyond)."""
+    r = np.arange(row0, row0 + rows, dtype=np.uint64)[:, None]
+    c = np.arange(col0, col0 + cols, dtype=np.uint64)[None, :]
+    inside = (r < np.uint64(m)) & (c < np.uint64(m))
+    e = (r * np.uint64(m) + c).ravel()
+    o = philox4x64_10(e >> np.uint64(2), seed)
+    q = ((e & np.uint64(3)) >> np.uint64(1)).astype(np.int64)
+    a = o[np.arange(e.size), 2 * q]
+    bb = o[np.arange(e.size), 2 * q + 1]
+    u1 = ((a >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+    u2 = (bb >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    rho = np.sqrt(-2.0 * np.log(u1))
+    theta = 6.283185307179586 * u2
+    g = rho * np.where((e & np.uint64(1)) == 1, np.sin(theta), np.cos(theta))
+    g = g.reshape(rows, cols)
+    diag = r == c
+    g = np.where(diag, g + shift, g)
+    return np.where(inside, g, np.where(diag, 1.0, 0.0))

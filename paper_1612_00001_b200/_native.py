@@ -40,6 +40,10 @@ SIGNATURES = [
     ("bri_rbf_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_double, _c_double,
                                 _c_void_p, _c_void_p, _c_int, _P_INT]),
     ("bri_rbf_dense", _c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_double, _c_double, _c_void_p, _c_ll]),
+    ("bri_randn_blocks", _c_int, [_c_void_p, _c_void_p, _c_ll, ctypes.c_ulonglong, _c_double, _c_void_p,
+                                  _c_void_p, _c_int, _P_INT]),
+    ("bri_randn_window", _c_int, [_c_void_p, _c_ll, ctypes.c_ulonglong, _c_double, _c_ll, _c_ll, _c_int, _c_int,
+                                  _c_void_p, _c_ll]),
     ("bri_load_host_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _P_INT]),
     ("bri_schur_batch_gated", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_void_p, _c_void_p, _c_void_p]),
     ("bri_fp64_peak", _c_int, [_c_void_p, _c_int, ctypes.POINTER(_c_double)]),

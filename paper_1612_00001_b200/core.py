@@ -41,21 +41,28 @@ class Workspace:
     schedule: "dag" (default) evaluates each distinct reduction node once,
     level by level, batched on the device; "tree" follows the reference's
     depth-first evaluation one node at a time with its bounded footprint
-    (<= 2k + 4 live blocks).  Both return the same values.
+    (<= 2k + 4 live blocks).  "bounded" evaluates each distinct
+    node once in a low-footprint order within the device budget, spilling
+    node values to pinned host memory (bounded.py); "dag" switches to it by
+    itself when one target's DAG does not fit.  All return the same values.
     arena_bytes: device-memory budget of one run (default: 85% of free HBM).
+    host_bytes: pinned host memory a bounded run may use for spilled values
+    (default: 60% of the host's available memory).
     """
 
-    __slots__ = ("counters", "gauge", "executed", "schedule", "arena_bytes", "device")
+    __slots__ = ("counters", "gauge", "executed", "schedule", "arena_bytes", "host_bytes", "device")
 
     def __init__(self, counters: OpCounters | None = None, gauge: MemoryGauge | None = None, *,
-                 schedule: str = "dag", arena_bytes: int | None = None, device: int | None = None):
-        if schedule not in ("dag", "tree"):
-            raise ValueError(f"schedule must be 'dag' or 'tree', got {schedule!r}")
+                 schedule: str = "dag", arena_bytes: int | None = None, host_bytes: int | None = None,
+                 device: int | None = None):
+        if schedule not in ("dag", "tree", "bounded"):
+            raise ValueError(f"schedule must be 'dag', 'tree' or 'bounded', got {schedule!r}")
         self.counters = counters if counters is not None else OpCounters()
         self.gauge = gauge if gauge is not None else MemoryGauge()
         self.executed = OpCounters()
         self.schedule = schedule
         self.arena_bytes = arena_bytes
+        self.host_bytes = host_bytes
         self.device = device
 
     def adopt(self, buf) -> "Block":

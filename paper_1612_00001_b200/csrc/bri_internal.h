@@ -134,4 +134,17 @@ struct RbfArgs {
 cudaError_t launch_rbf(const RbfArgs& g, double* base, long long slot_elems, int ld, int bn, const int* items,
                        int count, cudaStream_t s);
 
+// Seeded Gaussian matrix M = G + shift I generated blockwise on the device (generate.cu).
+struct RandnArgs {
+  long long m;              // order of M (indices >= m are identity padding)
+  unsigned long long seed;  // Philox4x64-10 key word 0
+  double shift;             // added to the diagonal
+  const int* rmap;          // device view->global maps, or nullptr (identity)
+  const int* cmap;
+};
+// items: (block row, block col, slot) device triples of rows x cols blocks, or
+// nullptr = one rows x cols window at (row0, col0) written at base.
+cudaError_t launch_randn(const RandnArgs& g, double* base, long long slot_elems, int ld, int rows, int cols,
+                         long long row0, long long col0, const int* items, int count, cudaStream_t s);
+
 }  // namespace bri

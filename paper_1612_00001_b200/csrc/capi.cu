@@ -1125,6 +1125,33 @@ int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, dou
   return 0;
 }
 
+int bri_randn_blocks(bri_arena* ar, void* stream, long long m, unsigned long long seed, double shift,
+                     const int* rmap, const int* cmap, int count, const int* items) {
+  if (ar == nullptr || items == nullptr || m < 1 || count < 0 || (rmap == nullptr) != (cmap == nullptr))
+    return fail_msg("bri_randn_blocks: bad arguments");
+  if (count == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<int> h(items, items + 3 * count);
+  for (int q = 0; q < count; ++q)
+    if (h[3 * q] < 0 || h[3 * q + 1] < 0 || h[3 * q + 2] < 0 || h[3 * q + 2] >= ar->v.nslots)
+      return fail_msg("bri_randn_blocks: bad item");
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const RandnArgs g{m, seed, shift, rmap, cmap};
+  BRI_CHECK(launch_randn(g, ar->v.base, ar->v.slot_elems, ar->v.ld, ar->v.n, ar->v.n, 0, 0, dev, count, s));
+  return 0;
+}
+
+int bri_randn_window(void* stream, long long m, unsigned long long seed, double shift, long long row0,
+                     long long col0, int rows, int cols, double* out, long long ldo) {
+  if (out == nullptr || m < 1 || rows < 1 || cols < 1 || row0 < 0 || col0 < 0 || ldo < cols ||
+      ldo > 0x7fffffffLL)
+    return fail_msg("bri_randn_window: bad arguments");
+  const RandnArgs g{m, seed, shift, nullptr, nullptr};
+  BRI_CHECK(launch_randn(g, out, 0, (int)ldo, rows, cols, row0, col0, nullptr, 1, static_cast<cudaStream_t>(stream)));
+  return 0;
+}
+
 int bri_fp64_peak(void* stream, int iters, double* tflops) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int dev = 0, sms = 0;

@@ -142,3 +142,109 @@ cudaError_t launch_rbf(const RbfArgs& g, double* base, long long slot_elems, int
 }
 
 }  // namespace bri
+
+// ---------------------------------------------------------------------------
+// Seeded Gaussian test matrices generated blockwise on the device (BASELINE
+// config 5: M = G + m I, G i.i.d. N(0, 1) "generated blockwise from seed 4";
+// the reference has no blockwise scheme).
+//
+//   element (r, c), 0-based over order m:  e = r * m + c
+//   (o0, o1, o2, o3) = Philox4x64-10(counter = (e / 4, 0, 0, 0), key = (seed, 0))
+//     — numpy's np.random.Philox bit generator (Random123), restated here
+//   pair q = (e % 4) / 2:  u1 = ((o_{2q} >> 11) + 1) 2^-53 in (0, 1],
+//                          u2 = (o_{2q+1} >> 11) 2^-53 in [0, 1)
+//   Box-Muller: rho = sqrt(-2 log u1), theta = 2 pi u2,
+//               g = rho cos(theta) for even e, rho sin(theta) for odd e
+//   M_rc = g + (r == c ? shift : 0)
+//
+// Every element depends only on (seed, m, r, c), so any block (or any padded
+// window view) is produced independently and the matrix does not depend on
+// the partition k.  The integer stream is exact; log/sin/cos are CUDA's
+// (within 1-2 ulp of glibc's, which the numpy restatement uses).
+// ---------------------------------------------------------------------------
+namespace bri {
+namespace {
+
+__device__ __forceinline__ void philox4x64_10(unsigned long long c[4], unsigned long long k0,
+                                              unsigned long long k1) {
+  const unsigned long long M0 = 0xD2E7470EE14C6C93ULL, M1 = 0xCA5A826395121157ULL;
+  const unsigned long long W0 = 0x9E3779B97F4A7C15ULL, W1 = 0xBB67AE8584CAA73BULL;
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    const unsigned long long hi0 = __umul64hi(M0, c[0]), lo0 = M0 * c[0];
+    const unsigned long long hi1 = __umul64hi(M1, c[2]), lo1 = M1 * c[2];
+    const unsigned long long n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+    k0 += W0;
+    k1 += W1;
+  }
+}
+
+struct RandnParams {
+  long long m;
+  unsigned long long seed;
+  double shift;
+  const int* rmap;  // view index -> global index (nullptr: identity)
+  const int* cmap;
+};
+
+__device__ __forceinline__ double randn_element(const RandnParams& p, long long r, long long c) {
+  if (r >= p.m || c >= p.m) return r == c ? 1.0 : 0.0;  // identity padding [[M, 0], [0, I]]
+  const unsigned long long e = (unsigned long long)r * (unsigned long long)p.m + (unsigned long long)c;
+  unsigned long long ctr[4] = {e >> 2, 0ULL, 0ULL, 0ULL};
+  philox4x64_10(ctr, p.seed, 0ULL);
+  const int q = (int)(e & 3ULL) >> 1;
+  const unsigned long long a = q ? ctr[2] : ctr[0], bb = q ? ctr[3] : ctr[1];
+  const double u1 = __dmul_rn((double)((a >> 11) + 1ULL), 0x1.0p-53);
+  const double u2 = __dmul_rn((double)(bb >> 11), 0x1.0p-53);
+  const double rho = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+  const double theta = __dmul_rn(6.283185307179586, u2);
+  const double g = __dmul_rn(rho, (e & 1ULL) ? sin(theta) : cos(theta));
+  return r == c ? __dadd_rn(g, p.shift) : g;
+}
+
+// grid.y = item; each CTA strides over the block's rows x cols elements.
+__global__ void __launch_bounds__(256) randn_kernel(RandnParams p, double* base, long long slot_elems, int ld,
+                                                    int rows, int cols, long long row0, long long col0,
+                                                    const int* items) {
+  double* out = base;
+  long long r0 = row0, c0 = col0;
+  if (items != nullptr) {
+    const int* it = items + 3 * blockIdx.y;
+    r0 = (long long)it[0] * rows;
+    c0 = (long long)it[1] * cols;
+    out = base + (long long)it[2] * slot_elems;
+  }
+  const long long total = (long long)rows * cols;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / cols), c = (int)(idx % cols);
+    const long long vr = r0 + r, vc = c0 + c;
+    const long long gr = p.rmap != nullptr ? (long long)p.rmap[vr] : vr;
+    const long long gc = p.cmap != nullptr ? (long long)p.cmap[vc] : vc;
+    out[(long long)r * ld + c] = randn_element(p, gr, gc);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_randn(const RandnArgs& g, double* base, long long slot_elems, int ld, int rows, int cols,
+                         long long row0, long long col0, const int* items, int count, cudaStream_t s) {
+  if (count > 65535 || rows < 1 || cols < 1) return cudaErrorInvalidValue;
+  RandnParams p{g.m, g.seed, g.shift, g.rmap, g.cmap};
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long total = (long long)rows * cols;
+  long long want = (total + 255) / 256;
+  const long long cap = (long long)sms * 8 / (count > 0 ? count : 1) + 1;
+  const unsigned gx = (unsigned)(want < cap ? want : cap);
+  count_launch();
+  randn_kernel<<<dim3(gx, count), 256, 0, s>>>(p, base, slot_elems, ld, rows, cols, row0, col0, items);
+  return cudaGetLastError();
+}
+
+}  // namespace bri

@@ -108,6 +108,13 @@ class Arena:
             self.gauge.on_alloc()
         return s
 
+    def claim(self, s: int) -> None:
+        """Take a specific free slot (plans that assign slots themselves, bounded.py)."""
+        self._free.remove(s)
+        self._live.add(s)
+        if self.gauge is not None:
+            self.gauge.on_alloc()
+
     def release(self, s: int) -> None:
         self._live.remove(s)
         self._free.append(s)
@@ -221,6 +228,16 @@ class Arena:
             ctypes.c_void_p(rmap.data_ptr()) if rmap is not None else None,
             ctypes.c_void_p(cmap.data_ptr()) if cmap is not None else None, len(items), self._items(flat)),
             "bri_rbf_blocks")
+
+    def randn(self, spec, items, rmap=None, cmap=None) -> None:
+        """Generate view blocks of a providers.GaussianSpec matrix into slots: items
+        (block row, block col, slot), 0-based; rmap/cmap int32 device tensors or None."""
+        flat = [s for it in items for s in it]
+        _native.check(self.lib.bri_randn_blocks(
+            self.handle, self.stream, spec.order, spec.seed, float(spec.shift),
+            ctypes.c_void_p(rmap.data_ptr()) if rmap is not None else None,
+            ctypes.c_void_p(cmap.data_ptr()) if cmap is not None else None, len(items), self._items(flat)),
+            "bri_randn_blocks")
 
     def close(self) -> None:
         if getattr(self, "handle", None) is not None:

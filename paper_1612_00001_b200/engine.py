@@ -166,8 +166,8 @@ class _WindowSource:
 
 
 class _GenSource:
-    """Generated providers (LS-SVM kernel matrix): blocks computed straight
-    into their slots on the device; maps select a padded window view."""
+    """Generated providers (LS-SVM kernel matrix, seeded Gaussian matrix): blocks
+    computed straight into their slots on the device; maps select a padded window view."""
 
     def __init__(self, gen, b: int, rmap, cmap, device: int):
         torch = _torch()
@@ -178,7 +178,7 @@ class _GenSource:
             self.cmap = torch.as_tensor(np.asarray(cmap, dtype=np.int32), device=f"cuda:{device}")
 
     def load(self, arena: Arena, items) -> None:
-        arena.rbf(self.gen, [(i - 1, j - 1, s) for i, j, s in items], self.rmap, self.cmap)
+        self.gen.fill(arena, [(i - 1, j - 1, s) for i, j, s in items], self.rmap, self.cmap)
 
 
 def _source_for(provider: BlockProvider, device: int):
@@ -214,6 +214,9 @@ class RunInfo:
     arena_slots: int = 0
     chunk: int = 0
     peak_blocks: int = 0
+    spills: int = 0          # bounded runs: device -> pinned host copies of node values
+    reloads: int = 0         # bounded runs: host -> device copies back
+    host_blocks: int = 0     # bounded runs: pinned host blocks used for spills
 
 
 class _TooBig(Exception):
@@ -434,6 +437,99 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
     return results, info
 
 
+_HOST_POOL: dict = {}
+
+
+def _pinned_pool(b: int, ld: int, count: int):
+    """Pinned host blocks for spilled values, kept across runs (pinning is slow)."""
+    torch = _torch()
+    pool = _HOST_POOL.setdefault((b, ld), [])
+    while len(pool) < count:
+        pool.append(torch.empty((b, ld), dtype=torch.float64, pin_memory=True))
+    return pool
+
+
+def release_host_pool() -> None:
+    """Unpin and free the spill buffers of bounded runs."""
+    _HOST_POOL.clear()
+
+
+def _host_slots(ws: Workspace, b: int) -> int:
+    ld = padded_ld(b)
+    blk = b * ld * 8
+    if ws.host_bytes is not None:
+        return ws.host_bytes // blk
+    import psutil
+
+    pooled = len(_HOST_POOL.get((b, ld), ())) * blk
+    return int((psutil.virtual_memory().available * 0.6 + pooled) // blk)
+
+
+def _run_bounded(src, sched, ws: Workspace, device: int, trace=None, invert_roots=True):
+    """Evaluate every DAG node once within the device budget (bounded.py): nodes run
+    one at a time in a low-footprint order; base blocks are loaded when a node needs
+    them; values evicted from the arena go to pinned host blocks and come back before
+    their next reader.  All copies are on the run's stream, in plan order."""
+    from . import bounded as bd
+
+    torch = _torch()
+    b = src.b
+    nroots = len(sched.specs)
+    p = bd.best_plan(sched, _budget_slots(ws, b, device), max_host=_host_slots(ws, b),
+                     invert_roots=invert_roots)
+    nslots = bd.slots_used(p)
+    info = RunInfo("bounded", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),
+                   {n: len(v) for n, v in sched.levels().items()}, nslots, 1,
+                   spills=p.spills, reloads=p.reloads, host_blocks=p.host_buffers)
+    nst = max(1, len(sched.nodes))
+    st_all = torch.zeros(nst + max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
+    status, root_status = st_all[:nst], st_all[nst:]
+    results = [None] * nroots
+    host_vals = {}
+    arena = cached_arena(b, nslots, device, gauge=ws.gauge)
+    hbufs = _pinned_pool(b, arena.ld, p.host_buffers)
+    try:
+        for op in p.ops:
+            kind = op[0]
+            if kind == bd.NODE:
+                nid, items = op[1], op[2]
+                for s_ in items[4:]:
+                    arena.claim(s_)
+                arena.schur([items], status[nid:nid + 1])
+                if trace is not None:
+                    host_vals[nid] = arena.view(items[4]).cpu().numpy().copy()
+            elif kind == bd.FREE:
+                arena.release(op[1])
+            elif kind == bd.LOAD:
+                (i, j), s_ = op[1], op[2]
+                arena.claim(s_)
+                src.load(arena, [(i, j, s_)])
+            elif kind == bd.SPILL:
+                hbufs[op[3]].copy_(arena.tensor[op[2]], non_blocking=True)
+            elif kind == bd.RELOAD:
+                arena.claim(op[2])
+                arena.tensor[op[2]].copy_(hbufs[op[3]], non_blocking=True)
+            elif kind == bd.INVERT:
+                t, (r, f, o) = op[1], op[2]
+                arena.claim(f)
+                arena.claim(o)
+                arena.invert([(r, f, o)], root_status[t:t + 1])
+                results[t] = arena.view(o).clone()
+            elif kind == bd.OUTPUT:
+                results[op[1]] = arena.view(op[2]).clone()
+        st_host = st_all.cpu().numpy()  # synchronizes the stream
+        pstat = st_host[: len(sched.nodes)].astype(np.int64)
+        rstat = st_host[nst:nst + nroots] if invert_roots else None
+        if trace is not None and not pstat.any():
+            for t in range(nroots):
+                sched.walk(t, on_node=lambda nid, path, frame: trace(path, frame, host_vals[nid].copy()))
+        info.peak_blocks = ws.gauge.peak_blocks
+    finally:
+        arena.release_all()
+    sched.first_failure(pstat, rstat, b)
+    return results, info
+
+
 _SCHED_CACHE: "OrderedDict" = OrderedDict()
 
 
@@ -461,9 +557,11 @@ def _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots, key=Non
     try:
         tensors, info = _run_dag(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
         return tensors, info, [sched]
-    except _TooBig as e:
+    except _TooBig:
         if len(specs) == 1:
-            raise BadPartitionError(str(e)) from None
+            # one target whose DAG does not fit: same nodes, bounded footprint
+            tensors, info = _run_bounded(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
+            return tensors, info, [sched]
     h = len(specs) // 2
     p0 = paths0[:h] if paths0 is not None else None
     p1 = paths0[h:] if paths0 is not None else None
@@ -498,10 +596,13 @@ def _execute_padded(provider: BlockProvider, targets, ws: Workspace, trace=None)
         else:  # M does not fit in HBM: stream the view's blocks from the host
             src = _HostSource(view)
         sched = build_from_specs(lay.k, [(root_frame(lay.k), None, None)])
-        run = _run_tree if ws.schedule == "tree" else _run_dag
-        tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=True)
+        run = {"tree": _run_tree, "bounded": _run_bounded}.get(ws.schedule, _run_dag)
+        try:
+            tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=True)
+        except _TooBig:
+            tensors, info = _run_bounded(src, sched, ws, device, trace=trace, invert_roots=True)
         ws.counters.add_nodes(sched.tree_nodes(0), targets=1)
-        if ws.schedule == "dag":
+        if ws.schedule != "tree":
             ws.executed.add_nodes(len(sched.nodes), targets=1)
         else:
             ws.executed.block_inversions += 1
@@ -519,9 +620,10 @@ def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, inver
     k = base.layout.k
     specs = specs_fn(mr, mc)
     key = (k, tuple(targets)) if (targets is not None and mr is None and mc is None and paths0 is None) else None
-    if ws.schedule == "tree":
+    if ws.schedule in ("tree", "bounded"):
         sched = _schedule(key, k, specs, paths0)
-        tensors, info = _run_tree(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
+        run = _run_tree if ws.schedule == "tree" else _run_bounded
+        tensors, info = run(src, sched, ws, device, trace=trace, invert_roots=invert_roots)
         scheds = [sched]
     else:
         tensors, info, scheds = _run_grouped(src, k, specs, paths0, ws, device, trace, invert_roots, key)
@@ -532,7 +634,7 @@ def _execute(provider: BlockProvider, specs_fn, ws: Workspace, trace=None, inver
     # reference accounting (tree semantics), per root
     for t in range(len(sched.specs)):
         ws.counters.add_nodes(sched.tree_nodes(t), targets=1 if invert_roots else 0)
-    if ws.schedule == "dag":
+    if ws.schedule != "tree":
         ws.executed.add_nodes(executed_nodes, targets=len(sched.specs) if invert_roots else 0)
     elif invert_roots:
         ws.executed.block_inversions += len(sched.specs)

@@ -428,3 +428,39 @@ def test_lu_schedules_agree(bri, env, tmp_path):
         if key.startswith("err_"):
             assert got[key] <= 4 * ref[key] + 1e-13, (key, float(got[key]), float(ref[key]), env)
     assert rel_err(got["dense"], ref["dense"]) <= 1e-9
+
+
+def test_gaussian_provider_generated_on_device(bri):
+    """Config-5 input generator: device windows/blocks vs the numpy restatement (integer stream
+    exact; log/sin/cos within a few ulp), and BRI over generated blocks equals BRI over the same
+    bytes stored (resident, padded and bounded schedules)."""
+    import torch
+
+    from oracle import bri_oracle as orc
+
+    m, seed = 320, 4
+    spec = bri.GaussianSpec(m, seed, float(m))
+    dev = bri.gaussian_window(spec, 0, 0, m, m).cpu().numpy()
+    want = orc.gaussian_window(m, seed, float(m), 0, 0, m, m)
+    assert np.abs(dev - want).max() <= 1e-13
+    np.testing.assert_array_equal(bri.gaussian_window(spec, 17, 250, 40, 90).cpu().numpy(), dev[17:57, 250:340])
+    for k in (4, 8, 5):
+        prov = bri.make_gaussian_provider(spec, k)
+        ref = bri.make_memory_provider(dev, k)
+        for t in [(1, 1), (2, k)]:
+            np.testing.assert_array_equal(bri.invert_block(prov, *t).data, bri.invert_block(ref, *t).data)
+        np.testing.assert_array_equal(prov.fetch_block(2, 3).data, ref.fetch_block(2, 3).data)
+    sp7 = bri.GaussianSpec(300, seed, 300.0)  # m % k != 0: shifted-window views of generated blocks
+    d7 = bri.gaussian_window(sp7, 0, 0, 300, 300).cpu().numpy()
+    for t in [(1, 1), (3, 7)]:
+        x = bri.invert_block(bri.make_gaussian_provider(sp7, 7), *t).data
+        np.testing.assert_array_equal(x, bri.invert_block(bri.make_memory_provider(d7, 7), *t).data)
+    # config-5 shape (k = 8, one target) under a budget that forces the bounded schedule
+    b = 120
+    sp8 = bri.GaussianSpec(8 * b, seed, float(8 * b))
+    d8 = bri.gaussian_window(sp8, 0, 0, 8 * b, 8 * b).cpu().numpy()
+    ws = bri.Workspace(arena_bytes=12 * b * b * 8)
+    got, info = bri.invert_blocks(bri.make_gaussian_provider(sp8, 8), [(1, 1)], ws)
+    assert info.schedule == "bounded" and info.spills > 0
+    np.testing.assert_array_equal(got[0].cpu().numpy(), bri.invert_block(bri.make_memory_provider(d8, 8), 1, 1).data)
+    assert rel_err(got[0].cpu().numpy(), orc.invert_block(d8, 8, 1, 1, memo=True)) <= 1e-9

@@ -25,7 +25,7 @@ def _rel(x, y):
     return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
 
 
-@pytest.mark.parametrize("schedule", ["dag", "tree"])
+@pytest.mark.parametrize("schedule", ["dag", "tree", "bounded"])
 def test_worked_example(bri, golden, schedule):
     data, _ = golden
     prov = bri.make_memory_provider(np.array([[4.0, 2.0], [1.0, 3.0]]), 2)
@@ -38,7 +38,7 @@ def test_worked_example(bri, golden, schedule):
     assert ws.gauge.live_blocks == 0
 
 
-@pytest.mark.parametrize("schedule", ["dag", "tree"])
+@pytest.mark.parametrize("schedule", ["dag", "tree", "bounded"])
 def test_trace_4x4(bri, golden, schedule):
     data, meta = golden
     seen = {}
@@ -89,7 +89,7 @@ def test_spd_k2(bri, golden):
         assert _rel(out.data, data[f"spd_m{m}_t1_1"]) <= 1e-12
 
 
-@pytest.mark.parametrize("schedule", ["dag", "tree"])
+@pytest.mark.parametrize("schedule", ["dag", "tree", "bounded"])
 def test_singular_path(bri, golden, schedule):
     data, meta = golden
     with pytest.raises(bri.SingularPivotError) as exc:
@@ -180,7 +180,7 @@ def test_bounded_arena_groups_targets():
     """A DAG that does not fit the arena budget is split into target groups
     (engine._run_grouped); results equal the unbounded run bit for bit, the
     device footprint stays under the budget, and a single target that cannot
-    fit raises BadPartitionError."""
+    fit runs the bounded-footprint schedule instead."""
     import torch
 
     import paper_1612_00001_b200 as bri
@@ -201,5 +201,49 @@ def test_bounded_arena_groups_targets():
     assert ws.gauge.peak_blocks <= budget
     for x, y in zip(full, part):
         assert torch.equal(x, y)
+    one, info = bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=(need([(1, 1)]) - 10) * block))
+    assert info.schedule == "bounded" and torch.equal(one[0], full[0])
+
+
+@pytest.mark.parametrize("b,budget", [(128, 9), (128, 24), (64, 8), (200, 12)])
+def test_bounded_schedule_spills_bitwise(bri, b, budget):
+    """One config-5-shaped target (k=8) whose DAG does not fit: every node runs once within
+    `budget` device blocks, values spill to pinned host blocks and come back, and the
+    block equals the level-by-level DAG run bit for bit (and the oracle within 1e-9)."""
+    import torch
+
+    from oracle import bri_oracle as orc
+
+    a = shifted(8 * b, 41 + b)
+    prov = bri.make_memory_provider(a, 8)
+    want = bri.invert_block(prov, 1, 1).data
+    ld = (b + 7) // 8 * 8
+    ws = bri.Workspace(arena_bytes=budget * b * ld * 8)
+    got, info = bri.invert_blocks(prov, [(1, 1)], ws)
+    assert info.schedule == "bounded" and info.dag_nodes == 270 and info.spills > 0
+    assert ws.gauge.peak_blocks <= budget and ws.gauge.live_blocks == 0
+    assert ws.executed.schur_nodes == 270
+    np.testing.assert_array_equal(got[0].cpu().numpy(), want)
+    assert _rel(want, orc.invert_block(a, 8, 1, 1, memo=True)) <= 1e-9
     with pytest.raises(bri.BadPartitionError):
-        bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=(need([(1, 1)]) - 10) * block))
+        bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=budget * b * ld * 8, host_bytes=b * ld * 8))
+
+
+def test_bounded_schedule_many_targets_and_reduce_frame(bri):
+    """schedule='bounded' over several targets (roots inverted as soon as they exist) and
+    through reduce_frame (un-inverted roots) equals the DAG run bit for bit."""
+    import torch
+
+    a = shifted(6 * 104, 43)
+    prov = bri.make_memory_provider(a, 6)
+    targets = [(1, 1), (3, 2), (6, 6), (2, 5)]
+    x, _ = bri.invert_blocks(prov, targets)
+    ws = bri.Workspace(schedule="bounded", arena_bytes=10 * 104 * 104 * 8)
+    y, info = bri.invert_blocks(prov, targets, ws)
+    assert info.schedule == "bounded"
+    for u, v in zip(x, y):
+        assert torch.equal(u, v)
+    fr = bri.frame_at(6, (bri.Quadrant.A, bri.Quadrant.D))
+    r1 = bri.reduce_frame(prov, fr).data
+    r2 = bri.reduce_frame(prov, fr, bri.Workspace(schedule="bounded", arena_bytes=8 * 104 * 104 * 8)).data
+    np.testing.assert_array_equal(r1, r2)

@@ -236,3 +236,93 @@ def test_file_provider_blocks_match_memory(tmp_path):
         for al in range(1, k + 1):
             for be in range(1, k + 1):
                 np.testing.assert_array_equal(np.asarray(fil._block(al, be)), mem._block(al, be))
+
+
+def _replay_plan(sched, p, src):
+    """Interpret a bounded plan on the host with the oracle's fold: every slot's
+    content is tracked, so a node reading the wrong block or a slot written
+    while live fails here."""
+    from paper_1612_00001_b200 import bounded as bd
+
+    slot, hostbuf, out, done = {}, {}, {}, []
+    for op in p.ops:
+        kind = op[0]
+        if kind == bd.LOAD:
+            (i, j), s = op[1], op[2]
+            assert s not in slot and 0 <= s < p.nslots
+            slot[s] = (("m", i, j), src.block(i, j))
+        elif kind == bd.SPILL:
+            nid, s, hb = op[1], op[2], op[3]
+            assert slot[s][0] == ("v", nid)
+            hostbuf[hb] = slot[s]
+        elif kind == bd.RELOAD:
+            nid, s, hb = op[1], op[2], op[3]
+            assert s not in slot and hostbuf[hb][0] == ("v", nid)
+            slot[s] = hostbuf[hb]
+        elif kind == bd.FREE:
+            del slot[op[1]]
+        elif kind == bd.HFREE:
+            del hostbuf[op[1]]
+        elif kind == bd.NODE:
+            nid, items = op[1], op[2]
+            node = sched.nodes[nid]
+            want = [("m", r[1], r[2]) if r[0] == "m" else ("v", r[1]) for r in node.operands]
+            assert [slot[s][0] for s in items[:4]] == want
+            assert all(s not in slot for s in items[4:]) and len(set(items)) == 7
+            pv, rt, l_, r = (slot[s][1] for s in items[:4])
+            slot[items[4]] = (("v", nid), r - l_ @ (orc.invert_dense(pv) @ rt))
+            slot[items[5]] = slot[items[6]] = (None, None)
+            done.append(nid)
+        elif kind == bd.INVERT:
+            t, (r, f, o) = op[1], op[2]
+            assert slot[r][0] == ("v", sched.roots[t]) and f not in slot and o not in slot
+            out[t] = orc.invert_dense(slot[r][1])
+            slot[f] = slot[o] = (None, None)
+        elif kind == bd.OUTPUT:
+            out[op[1]] = slot[op[2]][1]
+        assert len(slot) <= p.nslots
+    assert sorted(done) == list(range(len(sched.nodes)))   # every node exactly once
+    assert not slot and not hostbuf                        # everything released
+    return out
+
+
+@pytest.mark.parametrize("m,k,nslots", [(24, 6, 7), (24, 6, 12), (56, 7, 9), (40, 5, 100)])
+def test_bounded_plan_reproduces_reference(m, k, nslots):
+    """The bounded-footprint plan (bounded.py) evaluates each DAG node once within nslots
+    device blocks and returns the reference's blocks bit for bit."""
+    from paper_1612_00001_b200 import bounded as bd
+
+    a = shifted(m, 2000 + m)
+    src = orc.BlockSource(a, k)
+    targets = [(1, 1), (2, k), (k, 3)]
+    sched = dag.build_schedule(k, targets)
+    p = bd.best_plan(sched, nslots)
+    assert bd.slots_used(p) <= nslots
+    out = _replay_plan(sched, p, src)
+    for t, (al, be) in enumerate(targets):
+        np.testing.assert_array_equal(out[t], orc.invert_block(a, k, al, be))
+    if nslots < 10:
+        assert p.spills > 0 and p.reloads >= p.spills
+    pu = bd.plan(sched, nslots, invert_roots=False)
+    out_u = _replay_plan(sched, pu, src)
+    for t in range(len(targets)):
+        np.testing.assert_array_equal(orc.invert_dense(out_u[t]), out[t])
+
+
+def test_bounded_plan_config5_footprint():
+    """Config 5 (k=8, one target, 270 nodes) at 45 device blocks of 3.36 GB: every node once,
+    at most 30 pinned host blocks; too small a host budget is refused up front."""
+    from paper_1612_00001_b200 import bounded as bd
+    from paper_1612_00001_b200.errors import BadPartitionError
+
+    sched = dag.build_schedule(8, [(1, 1)])
+    order = bd.low_footprint_order(sched)
+    assert sorted(order) == list(range(270))
+    assert bd.peak_live(sched, order) < sched.peak_level_blocks()
+    p = bd.best_plan(sched, 45)
+    assert p.host_buffers <= 30 and p.loads >= 64
+    assert sum(1 for op in p.ops if op[0] == bd.NODE) == 270
+    with pytest.raises(BadPartitionError):
+        bd.best_plan(sched, 45, max_host=5)
+    with pytest.raises(BadPartitionError):
+        bd.plan(sched, 6)

@@ -106,3 +106,27 @@ def test_kernel_matrix_oracle_matches_reference(golden):
     for name, n, d, gamma, sigma, k in meta["kernel"]:
         got = orc.kernel_matrix(data[f"kern_{name}_inputs"], gamma, sigma)
         np.testing.assert_array_equal(got, data[f"kern_{name}_matrix"])
+
+
+def test_philox_restatement_matches_numpy():
+    """The config-5 generator's integer stream is numpy's np.random.Philox (Philox4x64-10):
+    numpy increments the counter before each draw, so raw draw n is counter n + 1."""
+    for key in (0, 4, 2 ** 63 + 12345):
+        raw = np.random.Philox(key=np.array([key, 0], dtype=np.uint64)).random_raw(4 * 64)
+        np.testing.assert_array_equal(orc.philox4x64_10(np.arange(1, 65, dtype=np.uint64), key).ravel(), raw)
+
+
+def test_gaussian_window_properties():
+    """Blockwise Gaussian matrix: windows agree with the whole matrix (partition independent),
+    the shift lands on the diagonal only, padding is the identity, moments are N(0, 1)."""
+    m = 300
+    full = orc.gaussian_window(m, 4, 0.0, 0, 0, m, m)
+    np.testing.assert_array_equal(orc.gaussian_window(m, 4, 0.0, 37, 101, 50, 77), full[37:87, 101:178])
+    shifted_ = orc.gaussian_window(m, 4, float(m), 0, 0, m, m)
+    np.testing.assert_array_equal(shifted_ - np.diag(np.diag(shifted_)), full - np.diag(np.diag(full)))
+    np.testing.assert_array_equal(np.diag(shifted_), np.diag(full) + m)
+    pad = orc.gaussian_window(m, 4, 0.0, m - 2, m - 2, 4, 4)
+    np.testing.assert_array_equal(pad[2:, 2:], np.eye(2))
+    assert not pad[:2, 2:].any() and not pad[2:, :2].any()
+    assert abs(full.mean()) < 0.01 and abs(full.std() - 1.0) < 0.01
+    assert not np.array_equal(full, orc.gaussian_window(m, 5, 0.0, 0, 0, m, m))
