@@ -46,8 +46,8 @@ from .frames import PLAN, Frame, Quadrant, root_frame, split_frame
 from .instrumentation import OpCounters
 from .providers import BlockProvider
 
-__all__ = ["invert_block", "invert_block_row", "invert_full", "reduce_frame", "schur_eliminate",
-           "InversionSummary", "RunInfo"]
+__all__ = ["invert_block", "invert_block_row", "invert_blocks", "invert_blocks_sharded", "invert_full",
+           "reduce_frame", "schur_eliminate", "InversionSummary", "RunInfo"]
 
 
 def _torch():
@@ -528,6 +528,108 @@ def _run_bounded(src, sched, ws: Workspace, device: int, trace=None, invert_root
         arena.release_all()
     sched.first_failure(pstat, rstat, b)
     return results, info
+
+
+class _ArenaExecutor:
+    """Device executor of distributed.run_sharded: blocks are arena slots; received
+    operands land straight in slots (NCCL P2P into arena.tensor[s])."""
+
+    def __init__(self, arena: Arena, src, device: int, nnodes: int):
+        torch = _torch()
+        self.arena, self.src, self.b = arena, src, src.b
+        self.device = f"cuda:{device}"
+        self.st = torch.zeros(max(1, nnodes) + 1, dtype=torch.int32, device=self.device)
+        self.nodes_run = 0
+
+    def alloc(self):
+        return self.arena.alloc()
+
+    def tensor(self, h):
+        return self.arena.tensor[h]
+
+    def release(self, h):
+        self.arena.release(h)
+
+    def load(self, refs):
+        out = {ij: self.arena.alloc() for ij in refs}
+        self.src.load(self.arena, [(i, j, s) for (i, j), s in out.items()])
+        return out
+
+    def schur(self, items, nids):
+        torch = _torch()
+        scratch = [(self.arena.alloc(), self.arena.alloc()) for _ in items]
+        tmp = torch.zeros(len(items), dtype=torch.int32, device=self.device)
+        self.arena.schur([it + sc for it, sc in zip(items, scratch)], tmp)
+        self.st[torch.as_tensor(nids, device=self.device)] = tmp
+        for f, w in scratch:
+            self.arena.release(f)
+            self.arena.release(w)
+        self.nodes_run += len(items)
+
+    def invert(self, h):
+        f, o = self.arena.alloc(), self.arena.alloc()
+        st = self.st[-1:]
+        st.zero_()
+        self.arena.invert([(h, f, o)], st)
+        x = self.arena.view(o).clone()
+        self.arena.release(f)
+        self.arena.release(o)
+        return x, int(st.item())
+
+    def status(self, nids):
+        host = self.st.cpu().numpy()
+        return {nid: int(host[nid]) for nid in nids}
+
+    def empty_result(self):
+        torch = _torch()
+        return torch.empty((self.b, self.b), dtype=torch.float64, device=self.device)
+
+
+def invert_blocks_sharded(provider: BlockProvider, targets, ws: Workspace | None = None, group=None):
+    """Blocks `targets` of M^-1 over all ranks of the process group (one per GPU): ONE
+    deduplicated DAG over every target, each level's nodes dealt to ranks with operand
+    affinity, one NCCL P2P exchange of operand values per level, root blocks sent to rank 0
+    (distributed.run_sharded; "one exchange step per level").  Every node
+    runs once in the whole job, unlike target sharding, which repeats shared subtrees on
+    each rank.  Returns (tensors in target order on rank 0 / None elsewhere, RunInfo of this
+    rank); every rank raises the reference's error if a pivot fails."""
+    import torch.distributed as dist
+
+    from .distributed import assign_owners, rank_peak_blocks, run_sharded
+
+    if ws is None:
+        ws = Workspace()
+    device = ws.device if ws.device is not None else current_device()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    targets = [tuple(t) for t in targets]
+    lay = provider._base()[0].layout
+    for a_, b_ in targets:
+        _check_target(lay, a_, b_)
+    if lay.l != 0:
+        raise BadPartitionError("node-sharded runs need m % k == 0 (padded layouts run per target)")
+    src, base, mr, mc = _source_for(provider, device)
+    k = base.layout.k
+    specs = _target_specs(k, targets)(mr, mc)
+    key = (k, tuple(targets)) if (mr is None and mc is None) else None
+    sched = _schedule(key, k, specs, None)
+    owner = assign_owners(sched, world)
+    need = rank_peak_blocks(sched, owner, rank)
+    if need > _budget_slots(ws, src.b, device):
+        raise BadPartitionError(f"rank {rank} needs {need} blocks of order {src.b}; raise the budget or the rank count")
+    arena = cached_arena(src.b, need, device, gauge=ws.gauge)
+    ex = _ArenaExecutor(arena, src, device, len(sched.nodes))
+    try:
+        res, pstat, rstat = run_sharded(sched, rank, world, ex, group=group)
+    finally:
+        arena.release_all()
+    sched.first_failure(pstat, rstat, src.b)
+    for t in range(len(sched.specs)):
+        ws.counters.add_nodes(sched.tree_nodes(t), targets=1)
+    ws.executed.add_nodes(ex.nodes_run, targets=sum(1 for nid in sched.roots if owner[nid] == rank))
+    info = RunInfo("sharded", len(targets), len(sched.nodes), sum(sched.tree_nodes(t) for t in range(len(targets))),
+                   {n: len(v) for n, v in sched.levels().items()}, need, 0, ws.gauge.peak_blocks)
+    out = [res[t] for t in range(len(targets))] if res is not None else None
+    return out, info
 
 
 _SCHED_CACHE: "OrderedDict" = OrderedDict()

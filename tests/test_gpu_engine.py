@@ -247,3 +247,38 @@ def test_bounded_schedule_many_targets_and_reduce_frame(bri):
     r1 = bri.reduce_frame(prov, fr).data
     r2 = bri.reduce_frame(prov, fr, bri.Workspace(schedule="bounded", arena_bytes=8 * 104 * 104 * 8)).data
     np.testing.assert_array_equal(r1, r2)
+
+
+def test_node_sharded_device_executor_world1(bri, golden):
+    """invert_blocks_sharded on the device executor (NCCL process group of one rank: the
+    exchange is empty, the arena executor, status replay and root hand-off are exercised);
+    blocks equal the single-process DAG run bit for bit.  The multi-rank exchange itself is
+    covered on CPU (tests/test_multiproc.py, gloo)."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        a = shifted(6 * 128, 47)
+        prov = bri.make_memory_provider(torch.from_numpy(a).cuda(), 6)
+        targets = [(1, b) for b in range(1, 7)]
+        want, _ = bri.invert_blocks(prov, targets)
+        ws = bri.Workspace()
+        got, info = bri.invert_blocks_sharded(prov, targets, ws)
+        assert info.schedule == "sharded" and ws.executed.schur_nodes == info.dag_nodes
+        for x, y in zip(got, want):
+            assert torch.equal(x, y)
+        assert ws.gauge.live_blocks == 0
+        data, meta = golden
+        with pytest.raises(bri.SingularPivotError) as exc:
+            bri.invert_blocks_sharded(bri.make_memory_provider(data["singular_matrix"], 3), [(1, 1)])
+        assert [q.name for q in exc.value.path] == meta["singular"]["path"]
+    finally:
+        dist.destroy_process_group()

@@ -74,3 +74,162 @@ def test_shard_partition_covers_targets_once():
             seen += mine
         assert seen == tg
     assert shard_targets([(1, 1)], 1, 4) == ([(1, 1)], "weak")
+
+
+class _OracleExecutor:
+    """run_sharded executor on the host: the oracle's fold on torch CPU buffers (the device
+    executor is engine._ArenaExecutor; what is under test is the partition and the exchange)."""
+
+    device = "cpu"
+
+    def __init__(self, src, b):
+        import torch
+
+        self.torch, self.src, self.b = torch, src, b
+        self.bufs, self.next, self.st, self.peak = {}, 0, {}, 0
+
+    def alloc(self):
+        h = self.next
+        self.next += 1
+        self.bufs[h] = self.torch.empty((self.b, self.b), dtype=self.torch.float64)
+        self.peak = max(self.peak, len(self.bufs))
+        return h
+
+    def tensor(self, h):
+        return self.bufs[h]
+
+    def release(self, h):
+        del self.bufs[h]
+
+    def load(self, refs):
+        out = {}
+        for i, j in refs:
+            out[(i, j)] = h = self.alloc()
+            self.bufs[h].copy_(self.torch.from_numpy(self.src.block(i, j)))
+        return out
+
+    def schur(self, items, nids):
+        from oracle import bri_oracle as orc
+
+        for (p, rt, l_, r, o), nid in zip(items, nids):
+            pv, rtv, lv, rv = (self.bufs[h].numpy() for h in (p, rt, l_, r))
+            try:
+                self.bufs[o].copy_(self.torch.from_numpy(rv - lv @ (orc.invert_dense(pv) @ rtv)))
+            except orc.OracleSingular as e:
+                self.st[nid] = e.pivot_index
+                self.bufs[o].fill_(float("nan"))
+
+    def invert(self, h):
+        from oracle import bri_oracle as orc
+
+        try:
+            return self.torch.from_numpy(orc.invert_dense(self.bufs[h].numpy())), 0
+        except orc.OracleSingular as e:
+            return self.torch.full((self.b, self.b), float("nan"), dtype=self.torch.float64), e.pivot_index
+
+    def status(self, nids):
+        return {nid: self.st.get(nid, 0) for nid in nids}
+
+    def empty_result(self):
+        return self.torch.empty((self.b, self.b), dtype=self.torch.float64)
+
+
+def _node_worker(rank, world, port, m, k, targets, q, singular):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    from oracle import bri_oracle as orc
+    from paper_1612_00001_b200 import dag
+    from paper_1612_00001_b200.distributed import assign_owners, rank_peak_blocks, run_sharded
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a = np.load(singular) if singular else shifted(m, 9)
+    sched = dag.build_schedule(k, targets)
+    ex = _OracleExecutor(orc.BlockSource(a, k), m // k)
+    res, pst, rst = run_sharded(sched, rank, world, ex)
+    err = None
+    try:
+        sched.first_failure(pst, rst, m // k)
+    except Exception as e:  # every rank must raise the reference's error
+        err = (type(e).__name__, [q_.name for q_ in e.path] if hasattr(e, "path") else None)
+    mine = sum(1 for v in assign_owners(sched, world).values() if v == rank)
+    peak_ok = ex.peak <= rank_peak_blocks(sched, assign_owners(sched, world), rank, scratch=0)
+    if rank == 0:
+        q.put(("res", {t: v.numpy() for t, v in res.items()}, err, mine, peak_ok))
+    else:
+        q.put(("rank", None, err, mine, peak_ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,k,targets,world", [
+    (16, 8, [(1, 1)], 2),                       # config-5 shape: one deep target, 270 nodes
+    (24, 6, [(1, b) for b in range(1, 7)], 3),  # config-4 shape: a block row
+    (20, 5, "all", 2),                          # config-3 shape: every block
+])
+def test_node_sharded_dag_matches_reference(m, k, targets, world):
+    """One DAG over all targets, each level's nodes dealt to ranks, one operand exchange per
+    level (gloo here, NCCL P2P on GPUs): rank 0 gets every block bit-identical to the
+    reference recursion, every node runs on exactly one rank, and the per-rank footprint
+    stays within rank_peak_blocks."""
+    from oracle import bri_oracle as orc
+    from paper_1612_00001_b200 import dag
+
+    tg = [(x, y) for x in range(1, k + 1) for y in range(1, k + 1)] if targets == "all" else targets
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_node_worker, args=(r, world, port, m, k, tg, q, None)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res = next(g[1] for g in got if g[0] == "res")
+    assert all(g[2] is None and g[4] for g in got)
+    assert sum(g[3] for g in got) == len(dag.build_schedule(k, tg).nodes)
+    a = shifted(m, 9)
+    for t, (al, be) in enumerate(tg):
+        np.testing.assert_array_equal(res[t], orc.invert_block(a, k, al, be, memo=True))
+
+
+def test_node_sharded_singular_path(golden, tmp_path):
+    """A failing pivot on one rank is reported on every rank as the reference's
+    SingularPivotError path (statuses are all-reduced, then replayed)."""
+    data, meta = golden
+    f = tmp_path / "sing.npy"
+    np.save(f, data["singular_matrix"])
+    m = data["singular_matrix"].shape[0]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_node_worker, args=(r, 2, port, m, 3, [(1, 1)], q, str(f))) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for g in got:
+        assert g[2] == ("SingularPivotError", meta["singular"]["path"])
+
+
+def test_owner_assignment_balances_levels():
+    from paper_1612_00001_b200 import dag
+    from paper_1612_00001_b200.distributed import assign_owners, level_transfers
+
+    sched = dag.build_schedule(8, [(1, 1)])
+    for world in (1, 2, 4, 8):
+        own = assign_owners(sched, world)
+        for n, ids in sched.levels().items():
+            counts = [sum(1 for nid in ids if own[nid] == r) for r in range(world)]
+            assert max(counts) <= -(-len(ids) // world)
+        moved = sum(len(level_transfers(sched, own, ids)) for ids in sched.levels().values())
+        if world == 1:
+            assert moved == 0
+        # affinity keeps traffic well below "every operand moves"
+        assert moved <= 0.75 * sum(4 for nd in sched.nodes if nd.n > 2)
