@@ -16,8 +16,10 @@ roofline   : dominant kernel = the fused Schur GEMM (gemm_kernel, C = R - RT*W, 
              in this run by bri_fp64_peak (MEASURED_PEAKS.json has no FP64 entry).
 cpu_baseline: the oracle port (numpy/scipy = the reference's own LAPACK/BLAS calls) on this
              host's cores, one target per sample.
-Multi-GPU: targets are sharded across ranks (strong scaling, no data-path collective; results
-gathered to rank 0 over NCCL); a single-target config runs one replica per rank (weak).
+Multi-GPU: multi-target configs run one DAG with each level's nodes dealt to ranks and one NCCL
+P2P operand exchange per level (--shard nodes, default; strong scaling), or each rank its own
+chunk of targets gathered to rank 0 at the end (--shard targets); a single-target config runs
+one replica per rank (weak).
 """
 
 from __future__ import annotations
@@ -48,6 +50,9 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--b", type=int, default=None, help="override block order (proxy runs)")
     ap.add_argument("--schedule", default="dag", choices=["dag", "tree"])
+    ap.add_argument("--shard", default="nodes", choices=["nodes", "targets"],
+                    help="multi-GPU, multi-target configs: one DAG with its levels dealt to ranks "
+                         "(nodes) or each rank its own chunk of targets (targets)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -194,8 +199,13 @@ def run_ours(args):
     from paper_1612_00001_b200.distributed import gather_blocks, shard_targets
 
     my_targets, scaling = shard_targets(cfg["targets"], rank, world)
+    node_shard = world > 1 and len(cfg["targets"]) > 1 and args.shard == "nodes"
+    if node_shard:  # one DAG for the job: every rank walks all targets, nodes dealt per level
+        my_targets = list(cfg["targets"])
     sched = build_schedule(k, my_targets)
     flops_rank = workloads.run_flops(b, len(sched.nodes), len(my_targets))
+    if node_shard:
+        flops_rank /= world   # summed over ranks below: the job's algorithmic FLOPs once
 
     a_dev = torch.from_numpy(a).to(f"cuda:{local}")
     prov = bri.make_memory_provider(a_dev, k)
@@ -203,6 +213,9 @@ def run_ours(args):
     ws = bri.Workspace(schedule=args.schedule)
 
     def step():
+        if node_shard:
+            tensors, _ = bri.invert_blocks_sharded(prov, my_targets, ws)
+            return tensors
         tensors, _ = bri.invert_blocks(prov, my_targets, ws)
         return tensors
 
@@ -239,7 +252,7 @@ def run_ours(args):
     value = flops_total / (ms_all * 1e-3) / 1e12
 
     # ---- gather results to rank 0 (strong scaling: the full inverse lands on rank 0)
-    if dist is not None and scaling == "strong":
+    if dist is not None and scaling == "strong" and not node_shard:
         gather_blocks(out, cfg["targets"], rank, world, b)
 
     # ---- end-to-end through the public API from pinned host memory
@@ -247,8 +260,12 @@ def run_ours(args):
 
     def e2e_step():
         p = bri.make_memory_provider(a_pin, k)
-        blocks = [bri.invert_block(p, *t, ws) for t in my_targets] if len(my_targets) == 1 else \
-            [bri.Block(x, ws) for x in bri.invert_blocks(p, my_targets, ws)[0]]
+        if node_shard:
+            res = bri.invert_blocks_sharded(p, my_targets, ws)[0] or []
+            blocks = [bri.Block(x, ws) for x in res]
+        else:
+            blocks = [bri.invert_block(p, *t, ws) for t in my_targets] if len(my_targets) == 1 else \
+                [bri.Block(x, ws) for x in bri.invert_blocks(p, my_targets, ws)[0]]
         host = [blk.data for blk in blocks]
         for blk in blocks:
             blk.release()
@@ -313,7 +330,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (PCG64 seeds of BASELINE.json configs)",
             "config": {"workload": f"config{args.config}", "k": k, "b": b, "m": k * b,
                        "targets": len(cfg["targets"]), "schedule": args.schedule,
-                       "dag_nodes_per_rank": len(sched.nodes),
+                       "dag_nodes_per_rank": len(sched.nodes) if not node_shard else None,
+                       "dag_nodes": len(sched.nodes),
+                       "shard": (args.shard if node_shard else "targets") if world > 1 else None,
                        "l2": "inputs larger than L2 (M = %.0f MiB > 126 MB)" % (a.nbytes / 2**20)},
             "pct_fp64_peak": 100.0 * value / (peak * world),
             "sec_per_block": (ms_all * 1e-3) / max(1, len(my_targets)) if scaling == "weak" else

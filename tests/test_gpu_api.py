@@ -443,7 +443,9 @@ def test_gaussian_provider_generated_on_device(bri):
     dev = bri.gaussian_window(spec, 0, 0, m, m).cpu().numpy()
     want = orc.gaussian_window(m, seed, float(m), 0, 0, m, m)
     assert np.abs(dev - want).max() <= 1e-13
-    np.testing.assert_array_equal(bri.gaussian_window(spec, 17, 250, 40, 90).cpu().numpy(), dev[17:57, 250:340])
+    np.testing.assert_array_equal(bri.gaussian_window(spec, 17, 250, 40, 70).cpu().numpy(), dev[17:57, 250:320])
+    pad = bri.gaussian_window(spec, m - 3, m - 3, 6, 6).cpu().numpy()  # identity padding beyond m
+    np.testing.assert_array_equal(pad[3:, 3:], np.eye(3))
     for k in (4, 8, 5):
         prov = bri.make_gaussian_provider(spec, k)
         ref = bri.make_memory_provider(dev, k)

@@ -28,6 +28,36 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def neumann_y11(m: int, k: int, b: int, seed: int, terms: int):
+    """Top block of the first block column of M^-1 = (1/m) sum_j (-G/m)^j for M = G + m I
+    (GaussianSpec(m, seed, m)), by c_0 = E_1, c_{j+1} = G c_j on generated G blocks with the
+    library's batched GEMM.  Returns (Y_11 device tensor, last term's max / max|Y_11|)."""
+    import torch
+
+    import paper_1612_00001_b200 as bri
+    from paper_1612_00001_b200.device import Arena
+
+    ar = Arena(b, 3 * k, device=0)
+    c_cur, c_nxt, gcol = list(range(0, k)), list(range(k, 2 * k)), list(range(2 * k, 3 * k))
+    y11 = torch.eye(b, dtype=torch.float64, device="cuda:0") / m            # j = 0: E_1 / m
+    g_only = bri.GaussianSpec(m, seed, 0.0)
+    ar.randn(g_only, [(i, 0, c_cur[i]) for i in range(k)])                 # c_1 = G E_1 = G[:, 1]
+    y11.add_(ar.view(c_cur[0]), alpha=-1.0 / float(m) ** 2)
+    for j in range(2, terms + 1):
+        ar.tensor[c_nxt[0]:c_nxt[-1] + 1].zero_()
+        for jb in range(k):                      # c_j = G c_{j-1}, one block column of G at a time
+            ar.randn(g_only, [(i, jb, gcol[i]) for i in range(k)])
+            # row-major C <- beta C + alpha B A with A = c_{j-1}[jb], B = G[i, jb]
+            ar.gemm([(c_cur[jb], gcol[i], c_nxt[i], c_nxt[i]) for i in range(k)], b, b, b,
+                    alpha=1.0, beta=0.0 if jb == 0 else 1.0)
+        c_cur, c_nxt = c_nxt, c_cur
+        y11.add_(ar.view(c_cur[0]), alpha=(-1.0) ** j / float(m) ** (j + 1))
+    torch.cuda.synchronize()
+    last = float(ar.view(c_cur[0]).abs().max()) / float(m) ** (terms + 1) / float(y11.abs().max())
+    ar.close()
+    return y11, last
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--b", type=int, default=20480)
@@ -43,7 +73,7 @@ def main():
 
     import paper_1612_00001_b200 as bri
     from paper_1612_00001_b200 import _native, engine, workloads
-    from paper_1612_00001_b200.device import Arena, fp64_peak_tflops, release_cached_memory
+    from paper_1612_00001_b200.device import fp64_peak_tflops, release_cached_memory
 
     torch.cuda.set_device(0)
     k, b = args.k, args.b
@@ -90,36 +120,14 @@ def main():
 
     # ---- Neumann-series block column of M^-1 on the device
     t1 = time.perf_counter()
-    ar = Arena(b, 3 * k, device=0)
-    c_cur = list(range(0, k))
-    c_nxt = list(range(k, 2 * k))
-    gcol = list(range(2 * k, 3 * k))
-    y11 = torch.eye(b, dtype=torch.float64, device="cuda:0") / m            # j = 0: E_1 / m
-    # c_1 = G E_1 = G[:, 1]  (the generated blocks of column 1 without the shift)
-    g_only = bri.GaussianSpec(m, args.seed, 0.0)
-    ar.randn(g_only, [(i, 0, c_cur[i]) for i in range(k)])
-    coef = -1.0 / m ** 2
-    y11.add_(ar.view(c_cur[0]), alpha=coef)
-    for j in range(2, args.terms + 1):
-        ar.tensor[c_nxt[0]:c_nxt[-1] + 1].zero_()
-        for jb in range(k):                      # c_{j} = G c_{j-1}, one block column of G at a time
-            ar.randn(g_only, [(i, jb, gcol[i]) for i in range(k)])
-            # row-major C <- beta C + alpha B A with A = c_{j-1}[jb], B = G[i, jb]
-            ar.gemm([(c_cur[jb], gcol[i], c_nxt[i], c_nxt[i]) for i in range(k)], b, b, b,
-                    alpha=1.0, beta=0.0 if jb == 0 else 1.0)
-        c_cur, c_nxt = c_nxt, c_cur
-        coef = (-1.0) ** j / float(m) ** (j + 1)
-        y11.add_(ar.view(c_cur[0]), alpha=coef)
-    torch.cuda.synchronize()
-    last = float(ar.view(c_cur[0]).abs().max()) / float(m) ** (args.terms + 1)
+    y11, last = neumann_y11(m, k, b, args.seed, args.terms)
     diff = float((x - y11).abs().max() / y11.abs().max())
     rec.update({
         "check": "Neumann series of M^-1 = (1/m) sum_j (-G/m)^j, block column 1, terms 0..%d" % args.terms,
-        "rel_diff_vs_neumann": diff, "last_term_rel": last / float(y11.abs().max()),
+        "rel_diff_vs_neumann": diff, "last_term_rel": last,
         "neumann_s": time.perf_counter() - t1,
         "x_diag_mean": float(x.diagonal().mean()), "one_over_m": 1.0 / m,
     })
-    ar.close()
     line = json.dumps(rec)
     print(line, flush=True)
     if args.out:
