@@ -136,6 +136,8 @@ def plan(sched, nslots: int, max_host: int | None = None, invert_roots: bool = T
     need = 7
     if nslots < need:
         raise BadPartitionError(f"a bounded DAG run needs at least {need} device blocks, the budget holds {nslots}")
+    # a plan never holds more than every value and base block at once
+    nslots = min(nslots, len(sched.nodes) + len(sched.m_blocks_used()) + 8)
     if order is None:
         order = low_footprint_order(sched)
     root_of = {}

@@ -475,7 +475,9 @@ def _run_bounded(src, sched, ws: Workspace, device: int, trace=None, invert_root
     torch = _torch()
     b = src.b
     nroots = len(sched.specs)
-    p = bd.best_plan(sched, _budget_slots(ws, b, device), max_host=_host_slots(ws, b),
+    # more slots than blocks the run ever holds would change nothing (and cost host time)
+    cap = len(sched.nodes) + len(sched.m_blocks_used()) + 8
+    p = bd.best_plan(sched, min(_budget_slots(ws, b, device), cap), max_host=_host_slots(ws, b),
                      invert_roots=invert_roots)
     nslots = bd.slots_used(p)
     info = RunInfo("bounded", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),

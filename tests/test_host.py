@@ -326,3 +326,17 @@ def test_bounded_plan_config5_footprint():
         bd.best_plan(sched, 45, max_host=5)
     with pytest.raises(BadPartitionError):
         bd.plan(sched, 6)
+
+
+def test_bounded_plan_huge_budget_is_capped():
+    """A budget of billions of tiny blocks (b = 1) plans in milliseconds: slots beyond what the
+    run can ever hold are not materialized."""
+    import time
+
+    from paper_1612_00001_b200 import bounded as bd
+
+    sched = dag.build_schedule(4, [(1, 1), (2, 2)])
+    t0 = time.perf_counter()
+    p = bd.plan(sched, 10 ** 10)
+    assert time.perf_counter() - t0 < 5 and p.spills == 0
+    assert bd.slots_used(p) <= len(sched.nodes) + len(sched.m_blocks_used()) + 8

@@ -65,6 +65,9 @@ def main():
     ap.add_argument("--seed", type=int, default=4)
     ap.add_argument("--terms", type=int, default=6)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--floor", action="store_true",
+                    help="also run BRI on M with its diagonal moved by one ulp (shift = nextafter(m)) and "
+                         "report max|X - X'| / max|X|: BRI's own 1-ulp sensitivity at this size")
     args = ap.parse_args()
 
     import numpy as np
@@ -128,6 +131,17 @@ def main():
         "neumann_s": time.perf_counter() - t1,
         "x_diag_mean": float(x.diagonal().mean()), "one_over_m": 1.0 / m,
     })
+    del y11
+    torch.cuda.empty_cache()
+    if args.floor:
+        import math
+
+        t2 = time.perf_counter()
+        spec_p = bri.GaussianSpec(m, args.seed, float(np.nextafter(float(m), math.inf)))
+        xp = bri.invert_blocks(bri.make_gaussian_provider(spec_p, k), [(1, 1)],
+                               bri.Workspace(host_bytes=int(psutil.virtual_memory().available * 0.8)))[0][0]
+        rec["floor_1ulp"] = float((xp - x).abs().max() / x.abs().max())
+        rec["floor_run_s"] = time.perf_counter() - t2
     line = json.dumps(rec)
     print(line, flush=True)
     if args.out:

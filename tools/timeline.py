@@ -21,11 +21,18 @@ ap.add_argument("--b", type=int, default=None)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--out", default="gpurun_out/timeline.json")
 ap.add_argument("--top", type=int, default=25)
+ap.add_argument("--gauss", action="store_true",
+                help="M = G + mI generated on the device (GaussianSpec seed 4, the config-5 input) instead "
+                     "of the config's host-generated matrix: large --b without a host GEMM")
 args = ap.parse_args()
 
 cfg = workloads.config(args.config, args.b)
-a = torch.from_numpy(workloads.make_matrix(args.config, args.b)).cuda()
-prov = bri.make_memory_provider(a, cfg["k"])
+if args.gauss:
+    m = cfg["k"] * cfg["b"]
+    prov = bri.make_gaussian_provider(bri.GaussianSpec(m, 4, float(m)), cfg["k"])
+else:
+    a = torch.from_numpy(workloads.make_matrix(args.config, args.b)).cuda()
+    prov = bri.make_memory_provider(a, cfg["k"])
 targets = cfg["targets"]
 for _ in range(args.warmup):
     bri.invert_blocks(prov, targets)
