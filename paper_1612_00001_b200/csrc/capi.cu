@@ -290,6 +290,14 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     return e ? atoi(e) : -1;
   }();
   const int fold_cap = fold_cap_env >= 0 ? fold_cap_env : (count <= 2 ? 48 : 0);
+  // The caps pay while the pivot chain is the critical path; for tall trailing
+  // matrices (n - J0 above this) the bulk update is, and every SM should take it.
+  static const int cap_rows_env = [] {
+    const char* e = getenv("BRI_CAP_ROWS");
+    return e ? atoi(e) : -1;
+  }();
+  const int cap_rows = cap_rows_env >= 0 ? cap_rows_env : 0x7fffffff;
+  auto capped = [&](int J0, int cap) { return (n - J0) <= cap_rows ? cap : 0; };
   // W <- L11^-1 P_J W on block J's rows, then W[N0:, :] -= L21 W[J rows, :]
   auto fold_block = [&](cudaStream_t st, int J0, int W, int pidx0, int npan) -> int {
     const bool tri = fold->tri;
@@ -307,7 +315,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, v, fold->fw, count, dl, true, J0, W, 0, ncol, tri, st));
     if (n - J0 - W > 0)
       return gemm_call(ar, st, fold->fwww, count, n - J0 - W, ncol, W, J0 + W, J0, J0, 0, J0 + W, 0, -1.0, 1.0,
-                       fold_cap);
+                       capped(J0, fold_cap));
     return 0;
   };
   double* du = dl + per * count;
@@ -321,7 +329,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(launch_rtrsm(v, fold->gf, count, du, J0, W, st));
     if (n - J0 - W > 0)
       return gemm_call(ar, st, fold->gfgg, count, n, n - J0 - W, W, 0, J0, J0, J0 + W, 0, J0 + W, -1.0, 1.0,
-                       fold_cap);
+                       capped(J0, fold_cap));
     return 0;
   };
   // C part of block J once its U row block is final (recorded as ev_b on s1)
@@ -387,7 +395,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N1, n, trail_cap)) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N1, n, capped(J0, trail_cap))) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
@@ -406,7 +414,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       }
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1 + WNN, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, trail_cap)) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, capped(J0, trail_cap))) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1 + WNN, WNN > 0 ? ctx->ev_x : nullptr)) return rc;

@@ -450,8 +450,13 @@ def _pinned_pool(b: int, ld: int, count: int):
 
 
 def release_host_pool() -> None:
-    """Unpin and free the spill buffers of bounded runs."""
+    """Unpin and free the spill buffers of bounded runs (also from PyTorch's pinned-memory cache,
+    which would otherwise keep them out of the host's available memory)."""
     _HOST_POOL.clear()
+    torch = _torch()
+    empty = getattr(torch._C, "_host_emptyCache", None)
+    if empty is not None:
+        empty()
 
 
 def _host_slots(ws: Workspace, b: int) -> int:

@@ -5,7 +5,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import rng, shifted
+from conftest import rel_err, rng, shifted
 
 pytestmark = pytest.mark.gpu
 
@@ -208,15 +208,18 @@ def test_bounded_arena_groups_targets():
 @pytest.mark.parametrize("b,budget", [(128, 9), (128, 24), (64, 8), (200, 12)])
 def test_bounded_schedule_spills_bitwise(bri, b, budget):
     """One config-5-shaped target (k=8) whose DAG does not fit: every node runs once within
-    `budget` device blocks, values spill to pinned host blocks and come back, and the
-    block equals the level-by-level DAG run bit for bit (and the oracle within 1e-9)."""
+    `budget` device blocks, values spill to pinned host blocks and come back, and the block
+    equals the tree schedule (also one node per launch) bit for bit, the level-batched DAG run
+    within 1e-12 (batches of more than two factorizations take the unfolded LU variant, whose
+    rounding differs once b spans several outer blocks), and the oracle within 1e-9."""
     import torch
 
     from oracle import bri_oracle as orc
 
     a = shifted(8 * b, 41 + b)
     prov = bri.make_memory_provider(a, 8)
-    want = bri.invert_block(prov, 1, 1).data
+    want = bri.invert_block(prov, 1, 1, bri.Workspace(schedule="tree")).data
+    assert rel_err(bri.invert_block(prov, 1, 1).data, want) <= 1e-12
     ld = (b + 7) // 8 * 8
     ws = bri.Workspace(arena_bytes=budget * b * ld * 8)
     got, info = bri.invert_blocks(prov, [(1, 1)], ws)
@@ -224,7 +227,7 @@ def test_bounded_schedule_spills_bitwise(bri, b, budget):
     assert ws.gauge.peak_blocks <= budget and ws.gauge.live_blocks == 0
     assert ws.executed.schur_nodes == 270
     np.testing.assert_array_equal(got[0].cpu().numpy(), want)
-    assert _rel(want, orc.invert_block(a, 8, 1, 1, memo=True)) <= 1e-9
+    assert rel_err(want, orc.invert_block(a, 8, 1, 1, memo=True)) <= 1e-9
     with pytest.raises(bri.BadPartitionError):
         bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=budget * b * ld * 8, host_bytes=b * ld * 8))
 
