@@ -290,13 +290,16 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     return e ? atoi(e) : -1;
   }();
   const int fold_cap = fold_cap_env >= 0 ? fold_cap_env : (count <= 2 ? 48 : 0);
-  // The caps pay while the pivot chain is the critical path; for tall trailing
-  // matrices (n - J0 above this) the bulk update is, and every SM should take it.
+  // The caps pay while the pivot chain is the critical path (n <= 4096); for
+  // larger orders the bulk updates are, and every SM should take them:
+  // measured on one node + inversion (tools/sweep_caps_large.sh), uncapped vs
+  // capped: b = 8192 193.5 -> 166.4 ms, b = 20480 2685 -> 2242 ms; per-block
+  // capping once n - J0 <= 4096 (BRI_CAP_ROWS=4096) measured 170 / 2277 ms.
   static const int cap_rows_env = [] {
     const char* e = getenv("BRI_CAP_ROWS");
     return e ? atoi(e) : -1;
   }();
-  const int cap_rows = cap_rows_env >= 0 ? cap_rows_env : 0x7fffffff;
+  const int cap_rows = cap_rows_env >= 0 ? cap_rows_env : (n > 4096 ? 0 : 0x7fffffff);
   auto capped = [&](int J0, int cap) { return (n - J0) <= cap_rows ? cap : 0; };
   // W <- L11^-1 P_J W on block J's rows, then W[N0:, :] -= L21 W[J rows, :]
   auto fold_block = [&](cudaStream_t st, int J0, int W, int pidx0, int npan) -> int {
