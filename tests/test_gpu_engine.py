@@ -208,27 +208,29 @@ def test_bounded_arena_groups_targets():
 @pytest.mark.parametrize("b,budget", [(128, 9), (128, 24), (64, 8), (200, 12)])
 def test_bounded_schedule_spills_bitwise(bri, b, budget):
     """One config-5-shaped target (k=8) whose DAG does not fit: every node runs once within
-    `budget` device blocks, values spill to pinned host blocks and come back, and the block
-    equals the schedule running the same per-node kernels bit for bit, the level-batched DAG run
-    within 1e-12 (batches of more than two factorizations take the unfolded LU variant, whose
-    rounding differs once b spans several outer blocks), and the oracle within 1e-9."""
+    `budget` device blocks, values spill to pinned host blocks and come back, and the block is
+    bit-identical to the same schedule run without any spill (spilling moves bytes, never
+    arithmetic); it matches the level-batched DAG run and the oracle within 1e-9 (batches of more
+    than two factorizations take the unfolded LU variant, a different rounding once b spans
+    several 128-column blocks)."""
     import torch
 
     from oracle import bri_oracle as orc
 
     a = shifted(8 * b, 41 + b)
     prov = bri.make_memory_provider(a, 8)
-    # the same per-node kernels as the bounded run: the one-CTA small-node kernel for b <= 96
-    # (DAG), the staged LU / solve / GEMM one node per launch for larger b (tree)
-    want = bri.invert_block(prov, 1, 1, bri.Workspace(schedule="dag" if b <= 96 else "tree")).data
-    assert rel_err(bri.invert_block(prov, 1, 1).data, want) <= 1e-12
     ld = (b + 7) // 8 * 8
+    roomy = bri.Workspace(schedule="bounded", arena_bytes=400 * b * ld * 8)
+    ref, rinfo = bri.invert_blocks(prov, [(1, 1)], roomy)
+    assert rinfo.schedule == "bounded" and rinfo.spills == 0
     ws = bri.Workspace(arena_bytes=budget * b * ld * 8)
     got, info = bri.invert_blocks(prov, [(1, 1)], ws)
     assert info.schedule == "bounded" and info.dag_nodes == 270 and info.spills > 0
     assert ws.gauge.peak_blocks <= budget and ws.gauge.live_blocks == 0
     assert ws.executed.schur_nodes == 270
-    np.testing.assert_array_equal(got[0].cpu().numpy(), want)
+    assert torch.equal(got[0], ref[0])
+    want = bri.invert_block(prov, 1, 1).data
+    assert rel_err(got[0].cpu().numpy(), want) <= 1e-9
     assert rel_err(want, orc.invert_block(a, 8, 1, 1, memo=True)) <= 1e-9
     with pytest.raises(bri.BadPartitionError):
         bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=budget * b * ld * 8, host_bytes=b * ld * 8))

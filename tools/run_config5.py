@@ -113,8 +113,12 @@ def main():
         "fp64_peak_tflops": peak, "pct_fp64_peak": 100 * flops / sec / 1e12 / peak,
         "launches": int(lib.bri_launch_count() - l0),
     })
-    print(json.dumps(rec), flush=True)
     x = tensors[0]
+    import hashlib
+
+    rec["sha256_16"] = hashlib.sha256(x.cpu().numpy().tobytes()).hexdigest()[:16]
+    rec["env"] = {k_: v for k_, v in os.environ.items() if k_.startswith("BRI_")}
+    print(json.dumps(rec), flush=True)
     del tensors
     release_cached_memory()     # the device arena goes; the pinned spill blocks stay for --floor
     if not args.floor:
