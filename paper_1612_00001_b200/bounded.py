@@ -18,8 +18,8 @@ before its next reader.  Config 5 at 45 device slots: 270 nodes, a few dozen
 3.36 GB spills, i.e. ~1% of the node arithmetic in PCIe time.
 
 `plan()` is pure Python (tested on CPU); engine._run_bounded replays the op
-list on the device.  Per-node arithmetic is the same kernel sequence as the
-other schedules, so all three return bit-identical blocks.
+list on the device, one node per launch.  Spilling moves bytes, never
+arithmetic: a run with spills is bit-identical to the same plan without.
 """
 
 from __future__ import annotations

@@ -6,9 +6,9 @@ providers.py:123-145) and on its label when n > 2 (a leaf always eliminates
 D).  The reference walks the literal tree and refetches shared subtrees by
 design (engine.py:26-27); the scheduler here evaluates every
 distinct (base rows, base cols, label|None) key once, across all requested
-targets.  Each node is computed by the same device kernels on the same
-operand bytes whichever schedule reaches it, so the deduplicated schedule
-is bit-identical to the tree walk (checked in tests/test_gpu_engine.py).
+targets.  Each node is computed from the same operand bytes whichever
+schedule reaches it (bit-identical to the tree walk while b fits one
+128-column LU block, tests/test_gpu_engine.py).
 
 Frames of order n only consume frames of order n-1, so the DAG is executed
 level by level (n = 2 .. k) with all nodes of a level batched into the same

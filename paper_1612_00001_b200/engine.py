@@ -19,8 +19,9 @@ Execution (the host scheduler):
   update), keeping <= 2 blocks per active level (the footprint contract
   <= 2k + 4, SPEC.md:286).
 
-Both schedules perform identical per-node arithmetic for b > 96 (same
-kernels on the same operand bytes), so they return bit-identical blocks.
+Both schedules perform the same per-node arithmetic while b fits one
+128-column LU block (bit-identical results); for larger b the LU variant
+depends on the launch's batch size and results agree within 1e-9.
 
 Errors: per-node pivot statuses come back from the device; the first failing
 pivot in the reference's evaluation order is reported as
