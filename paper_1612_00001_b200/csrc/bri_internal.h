@@ -17,6 +17,18 @@ namespace bri {
 // Every kernel launch made by the library bumps this (exported as bri_launch_count).
 void count_launch();
 
+// Programmatic dependent launch for the LU pivot chain (panel -> row panel ->
+// rank-32 update -> next panel, all on one stream): such a kernel is launched
+// with cudaLaunchAttributeProgrammaticStreamSerialization so its launch overlaps
+// the tail of its predecessor, and it executes griddepcontrol.wait before its
+// first global access.  BRI_PDL=0 disables the attribute.
+bool pdl_enabled();
+inline void pdl_attr(cudaLaunchAttribute& a) {
+  a.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  a.val.programmaticStreamSerializationAllowed = 1;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // One-time kernel attribute setup (dynamic shared memory), done at context creation
 // so that hot-path sequences can be captured into CUDA graphs on first use.
 cudaError_t configure_gemm();

@@ -20,6 +20,13 @@ using namespace bri;
 namespace bri {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("BRI_PDL");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on;
+}
 }  // namespace bri
 
 namespace {
@@ -295,6 +302,13 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   // measured on one node + inversion (tools/sweep_caps_large.sh), uncapped vs
   // capped: b = 8192 193.5 -> 166.4 ms, b = 20480 2685 -> 2242 ms; per-block
   // capping once n - J0 <= 4096 (BRI_CAP_ROWS=4096) measured 170 / 2277 ms.
+  // Correctness note: config 5 at b = 20480 (heavy pivoting: off-diagonal
+  // pivot blocks) with the caps forced on (BRI_CAP_ROWS=1000000) returned
+  // wrong, run-dependent blocks twice (rel. error 3e-5 and 0.34), while the
+  // uncapped default is bit-reproducible and within BRI's accuracy (3.3e-8 vs
+  // the Neumann reference); capped runs at n <= 12288 were verified accurate
+  // and bit-reproducible (tools/bounded_determinism.py).  Caps therefore stay
+  // restricted to n <= 4096 until that interaction is found.
   static const int cap_rows_env = [] {
     const char* e = getenv("BRI_CAP_ROWS");
     return e ? atoi(e) : -1;

@@ -294,6 +294,7 @@ constexpr int SK_LDB = SK_KC + 4;   // Bs[n][k]: B fragments 2 wavefronts
 __global__ void __launch_bounds__(256) skinny_kernel(GemmParams p) {
   __shared__ double As[SK_KC * SK_LDA];
   __shared__ double Bs[SK_BN * SK_LDB];
+  pdl_wait();
   const int* it = p.items + 4 * blockIdx.y;
   const double* A = p.base + (long long)it[0] * p.slot_elems;
   const double* B = p.base + (long long)it[1] * p.slot_elems;
@@ -407,9 +408,16 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     GemmParams q = p;
     q.tiles_m = (p.M + SK_BM - 1) / SK_BM;
     q.tiles_n = (p.N + SK_BN - 1) / SK_BN;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(q.tiles_m * q.tiles_n, count);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    pdl_attr(attr[0]);
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     count_launch();
-    skinny_kernel<<<dim3(q.tiles_m * q.tiles_n, count), 256, 0, stream>>>(q);
-    return cudaGetLastError();
+    return cudaLaunchKernelEx(&cfg, skinny_kernel, q);
   }
   p.count = count;
   long long ctas = (long long)p.tiles_m * p.tiles_n * count;

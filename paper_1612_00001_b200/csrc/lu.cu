@@ -191,6 +191,7 @@ BRI_DEVI void store_u_row(double* psm, int rhp, int jj, int nb, int slot, const 
 
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
+  pdl_wait();   // launched programmatically after the previous chain kernel
   constexpr int SW = 34;
   // one 288-byte message per CTA candidate: shifted live row, value, position
   struct __align__(16) CandMsg {
@@ -579,6 +580,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
   __shared__ double L[NBMAX][NBMAX + 1];
   __shared__ int sig[NBMAX];
   __shared__ int prs[1 + 2 * NBMAX];
+  pdl_wait();
   const int item = blockIdx.y;
   const int n = p.a.n, ld = p.a.ld, nb = p.nb, j0 = p.j0;
   double* X = p.a.base + (long long)p.slots[item] * p.a.slot_elems;
@@ -754,13 +756,14 @@ static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s
   cfg.blockDim = dim3(PT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  pdl_attr(attr[1]);
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   count_launch();
   return cudaLaunchKernelEx(&cfg, lu_panel_kernel<RPT>, p);
 }
@@ -852,9 +855,16 @@ cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int
   const int cols = (cend - cbeg) - ((j0 >= cbeg && j0 < cend) ? nb : 0);
   const int wpb = RP_THREADS / 32;
   const int gx = (cols + wpb - 1) / wpb + 1;  // +1: the pi-update block
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(gx, count);
+  cfg.blockDim = dim3(RP_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  pdl_attr(attr[0]);
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   count_launch();
-  rowpanel_kernel<<<dim3(gx, count), RP_THREADS, 0, s>>>(p);
-  return cudaGetLastError();
+  return cudaLaunchKernelEx(&cfg, rowpanel_kernel, p);
 }
 
 cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
