@@ -244,9 +244,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   const int n = v.n;
   bri_ctx* ctx = ar->ctx;
   cudaStream_t s1 = ctx->side;
-  BRI_CHECK(cudaMemsetAsync(sc.scale_bits, 0, (size_t)count * 8, s));
-  BRI_CHECK(cudaMemsetAsync(sc.pairs, 0, (size_t)count * L.pair_stride * 4, s));
-  BRI_CHECK(launch_pi_init(sc.pi, n, count, s));
+  BRI_CHECK(launch_pi_init(sc.pi, n, count, sc.scale_bits, sc.pairs, L.pair_stride, s));
   BRI_CHECK(launch_maxabs(v, dev_slots, count, sc.scale_bits, s));
   const int nbi = panel_width(n);
   const int outer = LU_OUTER;

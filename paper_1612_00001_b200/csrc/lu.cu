@@ -103,10 +103,15 @@ __global__ void identity_kernel(ArenaView a, const int* slots, int slot_stride) 
     for (int i = threadIdx.x; i < a.n; i += blockDim.x) x[i + (long long)j * a.ld] = (i == j) ? 1.0 : 0.0;
 }
 
-__global__ void pi_init_kernel(int* pi, int n) {
+// Per-factorization scratch reset: pi = identity, the panels' interchange lists
+// and the max|A| word zeroed (one kernel node instead of two graph memset nodes,
+// which the CUPTI timeline showed waiting ~0.5 ms behind the preceding kernel).
+__global__ void pi_init_kernel(int* pi, int n, unsigned long long* scale_bits, int* pairs, int pair_stride) {
   const int item = blockIdx.y;
-  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x)
-    pi[(long long)item * n + x] = x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  for (int x = tid; x < n; x += nth) pi[(long long)item * n + x] = x;
+  for (int x = tid; x < pair_stride; x += nth) pairs[(long long)item * pair_stride + x] = 0;
+  if (tid == 0) scale_bits[item] = 0ULL;
 }
 
 // ------------------------------------------------------------------ panel
@@ -738,9 +743,11 @@ cudaError_t launch_identity(const ArenaView& a, const int* slots, int slot_strid
   return cudaGetLastError();
 }
 
-cudaError_t launch_pi_init(int* pi, int n, int count, cudaStream_t s) {
+cudaError_t launch_pi_init(int* pi, int n, int count, unsigned long long* scale_bits, int* pairs, int pair_stride,
+                           cudaStream_t s) {
   count_launch();
-  pi_init_kernel<<<dim3((n + 255) / 256, count), 256, 0, s>>>(pi, n);
+  const int work = n > pair_stride ? n : pair_stride;
+  pi_init_kernel<<<dim3((work + 255) / 256, count), 256, 0, s>>>(pi, n, scale_bits, pairs, pair_stride);
   return cudaGetLastError();
 }
 
