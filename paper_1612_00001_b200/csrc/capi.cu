@@ -103,6 +103,14 @@ struct bri_ctx {
   DevBuf lu;      // LU scratch
   DevBuf dinv;    // inverted diagonal blocks of L and U (fused triangular solves)
   std::vector<int> host;  // staging for item arrays
+  // pinned staging ring for item uploads: a pageable source would make
+  // cudaMemcpyAsync wait for the stream to drain, so the host could not
+  // submit the next (large) graph while the GPU still runs the previous work
+  static constexpr int NSTAGE = 4;
+  void* stage[NSTAGE] = {};
+  size_t stage_bytes[NSTAGE] = {};
+  cudaEvent_t stage_ev[NSTAGE] = {};
+  int stage_next = 0;
 };
 
 struct bri_arena {
@@ -121,7 +129,23 @@ namespace {
 int upload(bri_ctx* ctx, cudaStream_t s, const std::vector<int>& h, int** dev) {
   const size_t bytes = h.size() * sizeof(int);
   if (int rc = ctx->items.ensure(bytes, s)) return rc;
-  BRI_CHECK(cudaMemcpyAsync(ctx->items.ptr, h.data(), bytes, cudaMemcpyHostToDevice, s));
+  const int k = ctx->stage_next;
+  ctx->stage_next = (k + 1) % bri_ctx::NSTAGE;
+  if (ctx->stage_ev[k] == nullptr) {
+    BRI_CHECK(cudaEventCreateWithFlags(&ctx->stage_ev[k], cudaEventDisableTiming));
+  } else {
+    BRI_CHECK(cudaEventSynchronize(ctx->stage_ev[k]));   // its previous copy has been read
+  }
+  if (ctx->stage_bytes[k] < bytes) {
+    if (ctx->stage[k] != nullptr) BRI_CHECK(cudaFreeHost(ctx->stage[k]));
+    ctx->stage[k] = nullptr;
+    const size_t nb = bytes + bytes / 2 + 4096;
+    BRI_CHECK(cudaHostAlloc(&ctx->stage[k], nb, cudaHostAllocDefault));
+    ctx->stage_bytes[k] = nb;
+  }
+  std::memcpy(ctx->stage[k], h.data(), bytes);
+  BRI_CHECK(cudaMemcpyAsync(ctx->items.ptr, ctx->stage[k], bytes, cudaMemcpyHostToDevice, s));
+  BRI_CHECK(cudaEventRecord(ctx->stage_ev[k], s));
   *dev = static_cast<int*>(ctx->items.ptr);
   return 0;
 }
@@ -725,6 +749,10 @@ void bri_ctx_destroy(bri_ctx* ctx) {
   if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
   if (ctx->ev_w) cudaEventDestroy(ctx->ev_w);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
+  for (int k = 0; k < bri_ctx::NSTAGE; ++k) {
+    if (ctx->stage[k]) cudaFreeHost(ctx->stage[k]);
+    if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);
+  }
   delete ctx;
 }
 
