@@ -64,6 +64,21 @@ void bri_arena_destroy(bri_arena* arena);
 int bri_schur_batch(bri_arena* arena, void* stream, int count, const int* items, int* status);
 
 /*
+ * One level of the deduplicated DAG with its shared work factored out —
+ * replaces engine.py:157-180 (_fold) for every node of the level.
+ *   fitems: nf pairs (p, F): F <- LU factors of p (dgetrf on the column-major view,
+ *           core.py:249); fstatus (device, nf ints): pivot test of p (core.py:200-209).
+ *   sitems: ns triples (f, l, W): W <- solve with factor f (0-based index into fitems)
+ *           of the right-hand side l (dgetrs, core.py:259), i.e. inv(p) applied to l.
+ *   gitems: ng quads (rt, W, r, out): out = r - rt (X) W (multiply + subtract,
+ *           core.py:173-197; out may alias r).
+ * In row-major block semantics each node's result is r - l @ inv(p) @ rt.
+ * Orders <= 96 are rejected (bri_schur_batch handles them in one kernel).
+ */
+int bri_level_batch(bri_arena* arena, void* stream, int nf, const int* fitems, int ns, const int* sitems, int ng,
+                    const int* gitems, int* fstatus);
+
+/*
  * Block inverses, batched — replaces core.py:238-263 (invert_dense).
  * items: 3 ints per block: slots (in, f, out); f is scratch; in is not modified.
  * status (device, count ints): pivot test of in.

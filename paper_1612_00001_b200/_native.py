@@ -47,6 +47,7 @@ SIGNATURES = [
     ("bri_load_host_blocks", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _P_INT]),
     ("bri_schur_batch_gated", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_void_p, _c_void_p, _c_void_p]),
     ("bri_fp64_peak", _c_int, [_c_void_p, _c_int, ctypes.POINTER(_c_double)]),
+    ("bri_level_batch", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT, _c_void_p]),
 ]
 
 _lib = None

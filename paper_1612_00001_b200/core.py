@@ -69,6 +69,12 @@ class Workspace:
         return Block(buf, self)
 
     def from_array(self, a, copy: bool = True) -> "Block":
+        torch = _torch()
+        if isinstance(a, torch.Tensor):   # device or host tensor: copied on the device side
+            t = a.to(device=_dev(self), dtype=torch.float64)
+            if copy and t.data_ptr() == a.data_ptr():
+                t = t.clone(memory_format=torch.contiguous_format)
+            return Block(t.contiguous(), self)
         return Block(np.array(a, dtype=np.float64, order="C", copy=True) if copy else a, self)
 
     def zeros(self, order: int) -> "Block":

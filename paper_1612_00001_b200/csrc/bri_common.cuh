@@ -147,6 +147,13 @@ BRI_DEVI void warp_argmax_fast(double& v, int& i) {
   v = (mi == 0x7fffffff) ? -1.0 : __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
 }
 
+// Value held by the lowest lane whose `owner` flag is set (0.0 if none): used
+// to carry a payload (e.g. the signed pivot) alongside warp_argmax_fast.
+BRI_DEVI double warp_pick(double v, bool owner) {
+  const unsigned m = __ballot_sync(0xffffffffu, owner);
+  return m ? __shfl_sync(0xffffffffu, v, __ffs(m) - 1) : 0.0;
+}
+
 // Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory into a
 // peer CTA's shared memory, completing `bytes` on the peer's mbarrier.
 BRI_DEVI void bulk_s2cluster(uint32_t dst_cluster, const void* src, uint32_t bytes, uint32_t mbar_cluster) {

@@ -97,7 +97,7 @@ cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
                           unsigned long long* scale_bits, cudaStream_t s);
 cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStream_t s);
 cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, const int* pi,
-                            int pi_stride, bool identity_src, cudaStream_t s);
+                            int pi_stride, bool identity_src, cudaStream_t s, const int* pidx = nullptr);
 cudaError_t launch_pi_init(int* pi, int n, int count, unsigned long long* scale_bits, int* pairs, int pair_stride,
                            cudaStream_t s);
 // dst X-column pi[x] = src X-column x (column scatter; X-columns are memory rows); pairs (src, dst)

@@ -1104,6 +1104,80 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
   return 0;
 }
 
+// One DAG level with its shared work factored out (engine._run_dag): in a level
+// of the deduplicated DAG many nodes share their pivot value (config 3: 6,499
+// nodes, 2,885 distinct pivots) and many share the pair (pivot, l) and hence
+// W = p^-1 l (3,902 distinct).  The reference evaluates each node on its own
+// (engine.py:157-180: invert_dense(p), multiply(inv, rt), multiply(l, t));
+// here each distinct pivot is factored once, each distinct W solved once, and
+// every node only pays its own fused GEMM-subtract.  Same kernels, same
+// operand bytes: each W and out is bit-identical to bri_schur_batch's large-
+// batch (unfolded) path.
+int bri_level_batch(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems, int ng,
+                    const int* gitems, int* fstatus) {
+  if (ar == nullptr || nf < 0 || ns < 0 || ng < 0 || (nf && !fitems) || (ns && !sitems) || (ng && !gitems))
+    return fail_msg("bri_level_batch: bad arguments");
+  if (nf == 0 && ns == 0 && ng == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = ar->v.n;
+  if (n <= SMALL_MAX) return fail_msg("bri_level_batch: order <= SMALL_MAX uses bri_schur_batch");
+  for (int i = 0; i < ns; ++i)
+    if (sitems[3 * i] < 0 || sitems[3 * i] >= nf) return fail_msg("bri_level_batch: solve names a bad factor");
+  // layout: [F (nf) | (p,F) (nf) | (F,F,F,F) (nf) | (F,F) (nf) | (l,W) (ns) | F_s (ns) | (F_s,W) (ns) |
+  //          (F_s,W,W,W) (ns) | fidx (ns) | (rt,W,r,out) (ng)]
+  std::vector<int> h;
+  h.reserve(9 * (size_t)nf + 10 * (size_t)ns + 4 * (size_t)ng);
+  auto F = [&](int f) { return fitems[2 * f + 1]; };
+  for (int f = 0; f < nf; ++f) h.push_back(F(f));
+  for (int f = 0; f < nf; ++f) { h.push_back(fitems[2 * f]); h.push_back(F(f)); }
+  for (int f = 0; f < nf; ++f) for (int q = 0; q < 4; ++q) h.push_back(F(f));
+  for (int f = 0; f < nf; ++f) { h.push_back(F(f)); h.push_back(F(f)); }
+  for (int i = 0; i < ns; ++i) { h.push_back(sitems[3 * i + 1]); h.push_back(sitems[3 * i + 2]); }
+  for (int i = 0; i < ns; ++i) h.push_back(F(sitems[3 * i]));
+  for (int i = 0; i < ns; ++i) { h.push_back(F(sitems[3 * i])); h.push_back(sitems[3 * i + 2]); }
+  for (int i = 0; i < ns; ++i) {
+    h.push_back(F(sitems[3 * i]));
+    for (int q = 0; q < 3; ++q) h.push_back(sitems[3 * i + 2]);
+  }
+  for (int i = 0; i < ns; ++i) h.push_back(sitems[3 * i]);
+  for (int g = 0; g < 4 * ng; ++g) h.push_back(gitems[g]);
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_f = dev;
+  const int* d_pf = dev + nf;
+  const int* d_ffff = dev + 3 * (size_t)nf;
+  const int* d_ff = dev + 7 * (size_t)nf;
+  const int* d_lw = dev + 9 * (size_t)nf;
+  const int* d_fs = d_lw + 2 * (size_t)ns;
+  const int* d_fw = d_fs + ns;
+  const int* d_fwww = d_fw + 2 * (size_t)ns;
+  const int* d_fidx = d_fwww + 4 * (size_t)ns;
+  const int* d_g = d_fidx + ns;
+  LuLayout L = lu_layout(n, nf > 0 ? nf : 1);
+  if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
+  if (int rc = ensure_dinv(ar, s, nf > ns ? nf : ns)) return rc;
+  LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  auto issue = [&](cudaStream_t st) -> int {
+    if (nf > 0) {
+      BRI_CHECK(launch_copy(ar->v, d_pf, nf, st));
+      if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, nf, L, sc)) return rc;
+    }
+    if (ns > 0) {   // W = U^-1 L^-1 P l with the permutation of the solve's factor
+      BRI_CHECK(launch_permcopy(ar->v, d_lw, ns, sc.pi, n, false, st, d_fidx));
+      if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false)) return rc;
+    }
+    if (ng > 0) return gemm_call(ar, st, d_g, ng, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
+    return 0;
+  };
+  std::vector<uintptr_t> key = graph_key(2, ar, ng, dev);
+  key.push_back((uintptr_t)nf);
+  key.push_back((uintptr_t)ns);
+  if (int rc = run_graphed(ar->ctx, s, key, issue)) return rc;
+  if (fstatus && nf > 0)
+    BRI_CHECK(cudaMemcpyAsync(fstatus, sc.status, (size_t)nf * 4, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
 int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ldm, int count,
                       const int* items) {
   if (ar == nullptr || M == nullptr || items == nullptr || count < 0) return fail_msg("bri_gather_blocks: bad arguments");

@@ -72,11 +72,12 @@ __global__ void copy_kernel(ArenaView a, const int* pairs) {
 // contiguous memory rows so both sides stay coalesced).  identity_src: the
 // source is the identity matrix (final block inversion, dgetrs against I).
 __global__ void permcopy_kernel(ArenaView a, const int* pairs, const int* pi, int pi_stride,
-                                int identity_src) {
+                                int identity_src, const int* pidx) {
   const int item = blockIdx.y;
   const double* src = a.base + (long long)pairs[2 * item] * a.slot_elems;
   double* dst = a.base + (long long)pairs[2 * item + 1] * a.slot_elems;
-  const int* p = pi + (long long)item * pi_stride;
+  // pidx (optional): item -> factor index whose permutation applies (shared factors)
+  const int* p = pi + (long long)(pidx ? pidx[item] : item) * pi_stride;
   for (int j = blockIdx.x; j < a.n; j += gridDim.x)
     for (int x = threadIdx.x; x < a.n; x += blockDim.x) {
       const int s = p[x];
@@ -465,9 +466,12 @@ struct TallArgs {
 __global__ void __launch_bounds__(PT, 1) lu_panel_tall_kernel(TallArgs p) {
   __shared__ double wv[PW];
   __shared__ int wi[PW];
+  __shared__ double ws[PW];
   __shared__ double cv[TALL_CS];
+  __shared__ double csg[TALL_CS];
   __shared__ int ci[TALL_CS];
   __shared__ int prow;
+  __shared__ double psig;
   const int cs = (int)cluster_nctarank();
   const int rank = (int)cluster_ctarank();
   const int item = blockIdx.x / cs;
@@ -481,36 +485,55 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_tall_kernel(TallArgs p) {
   for (int jj = 0; jj < nb; ++jj) {
     const int j = j0 + jj;
     double* colj = X + (long long)j * ld;        // X-column j = one memory row
-    // ---- argmax |X(i, j)| over i >= j (NaN never wins, smallest index on ties)
-    double bv = -1.0;
+    // ---- argmax |X(i, j)| over i >= j (NaN never wins, smallest index on ties).
+    // The SIGNED pivot value travels with its candidate through every level of
+    // the reduction: no thread reads X(pr, j) from memory after the winner is
+    // known, because rank 0 overwrites that element in the interchange below
+    // while lagging CTAs (or warps) could still be reading it.
+    double bv = -1.0, bs = 0.0;
     int bi = INT_MAX;
     for (int i = j + gtid; i < n; i += gthreads) {
-      const double v = fabs(colj[i]);
-      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; }
+      const double x = colj[i];
+      const double v = fabs(x);
+      if (v > bv || (v == bv && i < bi)) { bv = v; bi = i; bs = x; }
     }
-    warp_argmax_fast(bv, bi);
-    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+    {
+      const int mine = bi;
+      warp_argmax_fast(bv, bi);
+      bs = warp_pick(bs, mine == bi && bi != INT_MAX);
+    }
+    if (lane == 0) { wv[warp] = bv; wi[warp] = bi; ws[warp] = bs; }
     __syncthreads();
     if (warp == 0) {
-      double v = wv[lane % PW];
+      double v = wv[lane % PW], sg = ws[lane % PW];
       int i = wi[lane % PW];
+      const int mine = i;
       warp_argmax_fast(v, i);
+      sg = warp_pick(sg, mine == i && i != INT_MAX);
       if (lane < cs) {   // our CTA's candidate into slot `rank` of every CTA
         const uint32_t a = dsmem_addr(&cv[rank], lane), b = dsmem_addr(&ci[rank], lane);
+        const uint32_t c = dsmem_addr(&csg[rank], lane);
         asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
         asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(b), "r"(i) : "memory");
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(c), "d"(sg) : "memory");
       }
     }
     cluster_sync_all();
     if (warp == 0) {
-      double v = lane < cs ? cv[lane] : -1.0;
+      double v = lane < cs ? cv[lane] : -1.0, sg = lane < cs ? csg[lane] : 0.0;
       int i = lane < cs ? ci[lane] : INT_MAX;
+      const int mine = i;
       warp_argmax_fast(v, i);
-      if (lane == 0) prow = (i == INT_MAX) ? j : i;   // all NaN: pivot in place
+      sg = warp_pick(sg, mine == i && i != INT_MAX);
+      if (lane == 0) {
+        prow = (i == INT_MAX) ? j : i;   // all NaN: pivot in place (no interchange)
+        psig = sg;
+      }
     }
     __syncthreads();
     const int pr = prow;
-    const double piv = colj[pr];
+    // all-NaN column: pr == j, nothing is swapped, so X(j, j) is stable to read
+    const double piv = (pr == j) ? colj[j] : psig;
     if (tid == 0 && rank == 0) p.ipiv[(long long)item * p.n_stride + j] = pr;
     const bool swap = (pr != j && piv != 0.0);
     if (swap && rank == 0) {
@@ -721,10 +744,10 @@ cudaError_t launch_copy(const ArenaView& a, const int* pairs, int count, cudaStr
 }
 
 cudaError_t launch_permcopy(const ArenaView& a, const int* pairs, int count, const int* pi,
-                            int pi_stride, bool identity_src, cudaStream_t s) {
+                            int pi_stride, bool identity_src, cudaStream_t s, const int* pidx) {
   const int gx = a.n < 512 ? a.n : 512;
   count_launch();
-  permcopy_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs, pi, pi_stride, identity_src ? 1 : 0);
+  permcopy_kernel<<<dim3(gx, count), 256, 0, s>>>(a, pairs, pi, pi_stride, identity_src ? 1 : 0, pidx);
   return cudaGetLastError();
 }
 

@@ -67,6 +67,10 @@ def _torch_bytes(device: int):
         return torch.cuda.memory_reserved(device), torch.cuda.memory_allocated(device)
 
 
+# orders up to this run whole Schur nodes in one CTA (small.cu; csrc/bri_internal.h SMALL_MAX)
+SMALL_MAX = 96
+
+
 def padded_ld(n: int) -> int:
     return (n + 7) // 8 * 8
 
@@ -152,6 +156,15 @@ class Arena:
         flat = [s for it in items for s in it]
         _native.check(self.lib.bri_schur_batch(self.handle, self.stream, len(items), self._items(flat),
                                                ctypes.c_void_p(status.data_ptr())), "bri_schur_batch")
+
+    def level(self, fitems, sitems, gitems, fstatus) -> None:
+        """One DAG level with shared work (bri_level_batch): fitems (p, F) factor each distinct
+        pivot once, sitems (factor index, l, W) solve each distinct (pivot, l) once, gitems
+        (rt, W, r, out) one fused GEMM-subtract per node; fstatus: int32 device tensor (nf)."""
+        arr = lambda items: self._items([s for it in items for s in it]) if items else None
+        _native.check(self.lib.bri_level_batch(self.handle, self.stream, len(fitems), arr(fitems), len(sitems),
+                                               arr(sitems), len(gitems), arr(gitems),
+                                               ctypes.c_void_p(fstatus.data_ptr())), "bri_level_batch")
 
     def schur_gated(self, items, status, ev_l, ev_rtr) -> None:
         """schur() whose l / (rt, r) operands may still be in flight: the stream waits on

@@ -40,7 +40,7 @@ import numpy as np
 
 from .core import Block, Workspace
 from .dag import build_from_specs, build_schedule, target_maps
-from .device import Arena, cached_arena, cached_bytes, current_device, free_bytes, padded_ld
+from .device import SMALL_MAX, Arena, cached_arena, cached_bytes, current_device, free_bytes, padded_ld
 from .errors import (BadPartitionError, DimensionMismatchError, IndexOutOfRangeError,
                      SingularBlockError, SingularPivotError)
 from .frames import PLAN, Frame, Quadrant, root_frame, split_frame
@@ -218,6 +218,8 @@ class RunInfo:
     spills: int = 0          # bounded runs: device -> pinned host copies of node values
     reloads: int = 0         # bounded runs: host -> device copies back
     host_blocks: int = 0     # bounded runs: pinned host blocks used for spills
+    factorizations: int = 0  # DAG runs: pivot factorizations executed (shared across a level's nodes)
+    solves: int = 0          # DAG runs: W = p^-1 l solves executed (shared per distinct (pivot, l))
 
 
 class _TooBig(Exception):
@@ -288,26 +290,56 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
         else:
             src.load(arena, [(i, j, s) for (i, j), s in mslot.items()])
         val = {}
-        pos = {}
+        pos = {}      # node id -> position of its pivot status in `status`
+        pbase = 0
         prev = None
         for n, ids in levels.items():
             for c0 in range(0, len(ids), chunk):
                 part = ids[c0:c0 + chunk]
-                items, scratch = [], []
-                for nid in part:
-                    node = sched.nodes[nid]
-                    ops = [mslot[(r[1], r[2])] if r[0] == "m" else val[r[1]] for r in node.operands]
-                    out, f, w = arena.alloc(), arena.alloc(), arena.alloc()
-                    items.append((ops[0], ops[1], ops[2], ops[3], out, f, w))
-                    val[nid] = out
-                    pos[nid] = len(pos)
-                    scratch += (f, w)
-                base = pos[part[0]]
-                if gates is not None:
-                    arena.schur_gated(items, status[base:base + len(part)], *gates)
-                    gates = None
+                slot_of = lambda r: mslot[(r[1], r[2])] if r[0] == "m" else val[r[1]]
+                scratch = []
+                if b > SMALL_MAX and gates is None and len(part) > 2:
+                    # shared work: one factorization per distinct pivot, one solve per
+                    # distinct (pivot, l), one fused GEMM-subtract per node
+                    fidx, sidx, fitems, sitems, gitems = {}, {}, [], [], []
+                    for nid in part:
+                        refs = sched.nodes[nid].operands
+                        if refs[0] not in fidx:
+                            f = arena.alloc()
+                            fidx[refs[0]] = len(fitems)
+                            fitems.append((slot_of(refs[0]), f))
+                            scratch.append(f)
+                        sk = (refs[0], refs[2])
+                        if sk not in sidx:
+                            w = arena.alloc()
+                            sidx[sk] = w
+                            sitems.append((fidx[refs[0]], slot_of(refs[2]), w))
+                            scratch.append(w)
+                        out = arena.alloc()
+                        gitems.append((slot_of(refs[1]), sidx[sk], slot_of(refs[3]), out))
+                        val[nid] = out
+                        pos[nid] = pbase + fidx[refs[0]]
+                    arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)])
+                    pbase += len(fitems)
+                    info.factorizations += len(fitems)
+                    info.solves += len(sitems)
                 else:
-                    arena.schur(items, status[base:base + len(part)])
+                    items = []
+                    for nid in part:
+                        ops = [slot_of(r) for r in sched.nodes[nid].operands]
+                        out, f, w = arena.alloc(), arena.alloc(), arena.alloc()
+                        items.append((ops[0], ops[1], ops[2], ops[3], out, f, w))
+                        val[nid] = out
+                        pos[nid] = pbase + len(items) - 1
+                        scratch += (f, w)
+                    if gates is not None:
+                        arena.schur_gated(items, status[pbase:pbase + len(part)], *gates)
+                        gates = None
+                    else:
+                        arena.schur(items, status[pbase:pbase + len(part)])
+                    pbase += len(part)
+                    info.factorizations += len(part)
+                    info.solves += len(part)
                 for s in scratch:
                     arena.release(s)
             if not keep_all:
@@ -441,10 +473,16 @@ def _run_tree(src, sched, ws: Workspace, device: int, trace=None, invert_roots=T
 _HOST_POOL: dict = {}
 
 
-def _pinned_pool(b: int, ld: int, count: int):
+def _pool_key(device: int, b: int, ld: int):
+    # per device AND per thread, like _COPY_STREAMS: concurrent bounded runs of the same
+    # order from several threads (invert_full(jobs>1)) must not share spill buffers
+    return (device, threading.get_ident(), b, ld)
+
+
+def _pinned_pool(device: int, b: int, ld: int, count: int):
     """Pinned host blocks for spilled values, kept across runs (pinning is slow)."""
     torch = _torch()
-    pool = _HOST_POOL.setdefault((b, ld), [])
+    pool = _HOST_POOL.setdefault(_pool_key(device, b, ld), [])
     while len(pool) < count:
         pool.append(torch.empty((b, ld), dtype=torch.float64, pin_memory=True))
     return pool
@@ -460,14 +498,14 @@ def release_host_pool() -> None:
         empty()
 
 
-def _host_slots(ws: Workspace, b: int) -> int:
+def _host_slots(ws: Workspace, b: int, device: int) -> int:
     ld = padded_ld(b)
     blk = b * ld * 8
     if ws.host_bytes is not None:
         return ws.host_bytes // blk
     import psutil
 
-    pooled = len(_HOST_POOL.get((b, ld), ())) * blk
+    pooled = len(_HOST_POOL.get(_pool_key(device, b, ld), ())) * blk
     return int((psutil.virtual_memory().available * 0.6 + pooled) // blk)
 
 
@@ -483,7 +521,7 @@ def _run_bounded(src, sched, ws: Workspace, device: int, trace=None, invert_root
     nroots = len(sched.specs)
     # more slots than blocks the run ever holds would change nothing (and cost host time)
     cap = len(sched.nodes) + len(sched.m_blocks_used()) + 8
-    p = bd.best_plan(sched, min(_budget_slots(ws, b, device), cap), max_host=_host_slots(ws, b),
+    p = bd.best_plan(sched, min(_budget_slots(ws, b, device), cap), max_host=_host_slots(ws, b, device),
                      invert_roots=invert_roots)
     nslots = bd.slots_used(p)
     info = RunInfo("bounded", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),
@@ -495,7 +533,7 @@ def _run_bounded(src, sched, ws: Workspace, device: int, trace=None, invert_root
     results = [None] * nroots
     host_vals = {}
     arena = cached_arena(b, nslots, device, gauge=ws.gauge)
-    hbufs = _pinned_pool(b, arena.ld, p.host_buffers)
+    hbufs = _pinned_pool(device, b, arena.ld, p.host_buffers)
     try:
         for op in p.ops:
             kind = op[0]
