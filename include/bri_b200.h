@@ -42,6 +42,11 @@ int bri_version(void);
 /* Number of kernels this library has launched in the process so far. */
 long long bri_launch_count(void);
 
+/* Executed FLOPs this library has issued so far, per kernel family
+ * (0: GEMM kernels, 2*M*N*K per item; 1: triangular-solve leaves); -1 for a bad kind.
+ * Graph replays count what their kernels execute. */
+long long bri_flop_count(int kind);
+
 /* Message of the last failed call on this thread ("" if none). */
 const char* bri_last_error(void);
 

@@ -22,6 +22,7 @@ _P_INT = ctypes.POINTER(ctypes.c_int)
 SIGNATURES = [
     ("bri_version", _c_int, []),
     ("bri_launch_count", _c_ll, []),
+    ("bri_flop_count", _c_ll, [_c_int]),
     ("bri_last_error", ctypes.c_char_p, []),
     ("bri_ctx_create", _c_int, [_c_int, ctypes.POINTER(_c_void_p)]),
     ("bri_ctx_destroy", None, [_c_void_p]),

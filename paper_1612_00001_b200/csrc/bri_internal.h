@@ -16,6 +16,8 @@ namespace bri {
 
 // Every kernel launch made by the library bumps this (exported as bri_launch_count).
 void count_launch();
+enum { FLOP_GEMM = 0, FLOP_TRSM = 1, FLOP_KINDS = 2 };
+void count_flops(int kind, double flops);
 
 // Programmatic dependent launch for the LU pivot chain (panel -> row panel ->
 // rank-32 update -> next panel, all on one stream): such a kernel is launched

@@ -20,6 +20,17 @@ using namespace bri;
 namespace bri {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// Executed-FLOP ledger per kernel family (FLOP_GEMM: gemm/skinny/persistent
+// GEMM kernels, FLOP_TRSM: triangular-solve leaves): the numerator bench.py
+// divides by the family's in-step kernel time for the roofline.  Graph
+// replays add what their capture recorded (thread-local capture delta).
+static std::atomic<long long> g_flops[FLOP_KINDS];
+static thread_local long long tl_flops[FLOP_KINDS];
+void count_flops(int kind, double f) {
+  const long long v = (long long)f;
+  g_flops[kind].fetch_add(v, std::memory_order_relaxed);
+  tl_flops[kind] += v;
+}
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("BRI_PDL");
@@ -88,6 +99,7 @@ struct GraphEntry {
   std::vector<uintptr_t> key;
   cudaGraphExec_t exec;
   long long kernels;  // kernel nodes: counted as launches on every replay
+  long long flops[FLOP_KINDS];   // executed FLOPs per family: counted on every replay
 };
 
 struct bri_ctx {
@@ -212,6 +224,7 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
   p.c_c0 = c_c0;
   p.alpha = alpha;
   p.beta = beta;
+  count_flops(FLOP_GEMM, 2.0 * M * N * (double)K * count);
   BRI_CHECK(launch_gemm(ar->tmA, ar->tmB, p, count, s));
   return 0;
 }
@@ -569,10 +582,15 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
   if (hit != nullptr) {
     BRI_CHECK(cudaGraphLaunch(hit->exec, g));
     bri::g_launches.fetch_add(hit->kernels, std::memory_order_relaxed);
+    for (int q = 0; q < FLOP_KINDS; ++q) bri::count_flops(q, (double)hit->flops[q]);
   } else {
     {
+      long long f0[FLOP_KINDS];
+      for (int q = 0; q < FLOP_KINDS; ++q) f0[q] = bri::tl_flops[q];
       BRI_CHECK(cudaStreamBeginCapture(g, cudaStreamCaptureModeThreadLocal));
       rc = issue(g);
+      long long fcap[FLOP_KINDS];
+      for (int q = 0; q < FLOP_KINDS; ++q) fcap[q] = bri::tl_flops[q] - f0[q];
       cudaGraph_t graph = nullptr;
       const cudaError_t e = cudaStreamEndCapture(g, &graph);
       if (rc != 0) {
@@ -599,7 +617,9 @@ int run_graphed(bri_ctx* ctx, cudaStream_t s, const std::vector<uintptr_t>& key,
         cudaGraphExecDestroy(ctx->graphs.front().exec);
         ctx->graphs.erase(ctx->graphs.begin());
       }
-      ctx->graphs.push_back({key, exec, kernels});
+      GraphEntry ent{key, exec, kernels, {}};
+      for (int q = 0; q < FLOP_KINDS; ++q) ent.flops[q] = fcap[q];
+      ctx->graphs.push_back(ent);
       BRI_CHECK(cudaGraphLaunch(exec, g));
       // the captured launches went through count_launch() during capture
     }
@@ -702,6 +722,11 @@ extern "C" {
 int bri_version(void) { return 100; }
 
 long long bri_launch_count(void) { return bri::g_launches.load(std::memory_order_relaxed); }
+
+long long bri_flop_count(int kind) {
+  if (kind < 0 || kind >= bri::FLOP_KINDS) return -1;
+  return bri::g_flops[kind].load(std::memory_order_relaxed);
+}
 
 const char* bri_last_error(void) { return g_last_error.c_str(); }
 

@@ -437,6 +437,18 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
     return v;
   }();
   const bool fine = (long long)((nrhs + 31) / 32) * count <= sms;
+  // nr x nr triangle against nrhs columns (tri_rhs: column c starts at its diagonal)
+  double per = (double)nr * nr * nrhs;
+  if (tri_rhs) {
+    double t = 0.0;
+    for (int c = 0; c < nrhs; ++c) {
+      const int top = (c_off + c) > r0 ? (c_off + c) - r0 : 0;
+      const double h = top < nr ? (double)(nr - top) : 0.0;
+      t += h * h;
+    }
+    per = t;
+  }
+  count_flops(FLOP_TRSM, per * count);
   count_launch();
   if (fine) {
     dim3 grid((nrhs + 15) / 16, count);

@@ -29,13 +29,16 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _run(["--config", "1", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"])
+    d = _run(["--config", "3", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert key in d, key
     assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0
     r = d["roofline"]
-    assert r["bound"] in ("tensor", "hbm") and 0 < r["frac"] <= 1.2 and r["peak"] > 0
+    assert r["bound"] in ("tensor", "hbm") and 0 < r["frac"] <= 1.0 and r["peak"] > 0
+    assert r["kernel"] == "gemm_kernel" and 0 < r["step_share"] <= 1.0
+    assert d["config"]["workload"] == "config3" and d["config"]["targets"] == 64
+    assert 0 < d["executed"]["pct_fp64_peak"] <= 100.0
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
