@@ -23,8 +23,9 @@ import numpy as np
 
 from .errors import DimensionMismatchError, FormatError, IndexOutOfRangeError, MissingBlocksError
 
-__all__ = ["MemorySink", "BrimSink", "BrimHeader", "write_matrix", "read_header", "read_matrix",
-           "open_matrix", "MAGIC", "VERSION", "HEADER_BYTES"]
+__all__ = ["MemorySink", "BrimSink", "BrimHeader", "BrimReader", "write_matrix", "read_header", "read_matrix",
+           "open_matrix", "MAGIC", "VERSION", "HEADER_BYTES", "CSV_COLUMNS", "write_bench_csv",
+           "read_bench_csv"]
 
 MAGIC = b"BRIM"
 VERSION = 1
@@ -88,6 +89,67 @@ def open_matrix(path) -> np.ndarray:
 
 def read_matrix(path) -> np.ndarray:
     return np.array(open_matrix(path), dtype=np.float64)
+
+
+class BrimReader:
+    """Rectangle reads from a BRIM file (reference formats.py:127-176).
+
+    Served from a read-only memory map, so a rectangle costs its own pages and
+    concurrent readers need no seek lock; the header is validated on open."""
+
+    def __init__(self, path):
+        self.path = os.fspath(path)
+        self.header = read_header(self.path)
+        self._map = open_matrix(self.path)
+
+    @property
+    def m(self) -> int:
+        return self.header.m
+
+    def read_rect(self, r0: int, r1: int, c0: int, c1: int) -> np.ndarray:
+        m = self.header.m
+        if not (0 <= r0 <= r1 <= m and 0 <= c0 <= c1 <= m):
+            raise IndexOutOfRangeError(f"rectangle [{r0}:{r1}, {c0}:{c1}] outside order {m}")
+        if self._map is None:
+            raise FormatError(f"{self.path}: reader is closed")
+        return np.array(self._map[r0:r1, c0:c1], dtype=np.float64)
+
+    def close(self) -> None:
+        mm, self._map = self._map, None
+        if mm is not None and getattr(mm, "_mmap", None) is not None:
+            del mm
+
+    def __enter__(self) -> "BrimReader":
+        return self
+
+    def __exit__(self, exc_type, exc, tb) -> None:
+        self.close()
+
+
+# bench CSV (reference formats.py:285-318): one BenchRecord per row
+CSV_COLUMNS = ("method", "m", "k", "wall_ms", "peak_bytes", "n_block_inv", "n_block_mul", "seed")
+
+
+def write_bench_csv(path, records) -> None:
+    import csv
+
+    with open(os.fspath(path), "w", newline="") as fh:
+        out = csv.writer(fh)
+        out.writerow(CSV_COLUMNS)
+        out.writerows(rec.row() for rec in records)
+
+
+def read_bench_csv(path) -> list:
+    import csv
+
+    from .instrumentation import BenchRecord
+
+    types = (str, int, int, float, int, int, int, int)
+    with open(os.fspath(path), newline="") as fh:
+        rows = list(csv.reader(fh))
+    if not rows or tuple(rows[0]) != CSV_COLUMNS:
+        raise FormatError(f"{path}: bad bench CSV header {rows[0] if rows else None}")
+    return [BenchRecord(*(t(v) for t, v in zip(types, r))) for r in rows[1:] if r]
 
 
 def _as_host(block) -> np.ndarray:

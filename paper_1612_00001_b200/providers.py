@@ -30,7 +30,7 @@ from .errors import BadPartitionError, DimensionMismatchError, IndexOutOfRangeEr
 
 __all__ = ["BlockLayout", "BlockPermutation", "BlockProvider", "fetch_block", "make_memory_provider",
            "permute_provider", "window_maps", "window_finisher", "make_file_provider", "KernelSpec",
-           "make_kernel_provider", "kernel_matrix"]
+           "make_kernel_provider", "kernel_matrix", "augment_provider", "cache_provider"]
 
 
 @dataclass(frozen=True)
@@ -317,6 +317,96 @@ def fetch_block(provider: BlockProvider, alpha: int, beta: int, ws: Workspace | 
 def make_memory_provider(matrix, k: int) -> BlockProvider:
     """Provider over an in-memory square matrix (numpy array or torch tensor)."""
     return _MemoryProvider(matrix, k)
+
+
+class _SourceProvider(BlockProvider):
+    """Blocks of [[M, 0], [0, I]] from a user element source exposing `.m` and
+    `.rect(r0, r1, c0, c1)` (reference providers.py:318-336).  The engine reads it
+    block by block through its pinned host ring (no device copy of M exists)."""
+
+    def __init__(self, source, layout: BlockLayout):
+        if int(source.m) != layout.m:
+            raise DimensionMismatchError(f"source order {source.m} does not match layout order {layout.m}")
+        self.source = source
+        self.layout = layout
+
+    def _elements(self, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+        m = self.layout.m
+        out = np.zeros((rows.size, cols.size))
+        rr, cc = rows < m, cols < m
+        if rr.any() and cc.any():
+            r_in, c_in = rows[rr], cols[cc]
+            r0, r1, c0, c1 = int(r_in.min()), int(r_in.max()) + 1, int(c_in.min()), int(c_in.max()) + 1
+            rect = np.asarray(self.source.rect(r0, r1, c0, c1), dtype=np.float64)
+            out[np.ix_(rr, cc)] = rect[np.ix_(r_in - r0, c_in - c0)]
+        for i in np.flatnonzero(~rr):   # padding rows: the identity part of the augmentation
+            hit = np.flatnonzero(cols == rows[i])
+            if hit.size:
+                out[i, hit[0]] = 1.0
+        return out
+
+    def _block(self, alpha: int, beta: int) -> np.ndarray:
+        b = self.layout.b
+        idx_r = np.arange((alpha - 1) * b, alpha * b)
+        idx_c = np.arange((beta - 1) * b, beta * b)
+        return self._elements(idx_r, idx_c)
+
+    def run_view(self, alpha: int, beta: int):
+        return _augmented_run_view(self, alpha, beta)
+
+
+def augment_provider(source, layout: BlockLayout) -> BlockProvider:
+    """Padded block provider over an element source (reference providers.py:453-464)."""
+    return _SourceProvider(source, layout)
+
+
+class _CachedProvider(BlockProvider):
+    """Bounded LRU block cache in front of any provider (reference providers.py:417-450).
+
+    On this engine the device arena already keeps every block a run needs resident
+    (each base block is gathered once per run), so the cache only saves repeated host
+    reads across runs of a slow provider; fetches still return fresh buffers."""
+
+    def __init__(self, base: BlockProvider, capacity: int):
+        import threading
+        from collections import OrderedDict
+
+        if capacity < 1:
+            raise BadPartitionError(f"cache capacity must be >= 1, got {capacity}")
+        self.base = base
+        self.layout = base.layout
+        self.capacity = int(capacity)
+        self._lru: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
+        self._lock = threading.Lock()
+
+    def _block(self, alpha: int, beta: int) -> np.ndarray:
+        key = (alpha, beta)
+        with self._lock:
+            got = self._lru.get(key)
+            if got is not None:
+                self._lru.move_to_end(key)
+                return got.copy()
+        data = np.array(self.base._block(alpha, beta), dtype=np.float64)
+        with self._lock:
+            self._lru[key] = data
+            self._lru.move_to_end(key)
+            while len(self._lru) > self.capacity:
+                self._lru.popitem(last=False)
+        return data.copy()
+
+    def _elements(self, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+        return self.base._elements(rows, cols)
+
+    def run_view(self, alpha: int, beta: int):
+        view, finish = self.base.run_view(alpha, beta)
+        if finish is None:
+            return permute_provider(self, alpha, beta), None
+        return view, finish   # element windows bypass the block cache (as in the reference)
+
+
+def cache_provider(provider: BlockProvider, capacity: int) -> BlockProvider:
+    """Optional bounded LRU cache around any provider (reference providers.py:503-505)."""
+    return _CachedProvider(provider, capacity)
 
 
 class _FileProvider(_MemoryProvider):

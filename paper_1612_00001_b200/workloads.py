@@ -11,10 +11,12 @@ and the CPU oracle.
   cfg 4: k=16, b=2048,  G G^T / m + I (SPD),       seed 3, block row 1
   cfg 5: k=8,  b=20480, G + m I blockwise,         seed 4, block (1,1)
 
-cfg 5 (215 GB) needs a blockwise generator the reference does not have:
-block (i, j) is drawn from its own stream `SeedSequence(4).spawn` indexed
-row-major, plus m on the diagonal blocks' diagonals.  `scale` shrinks b for
-the proxies the survey used (e.g. cfg 5 at b=2048).
+cfg 5 (215 GB) needs a blockwise generator the reference does not have: the
+counter-based Philox4x64-10 + Box-Muller scheme of `GaussianSpec` /
+bri_randn_blocks (include/bri_b200.h), so a proxy at smaller b (e.g. b=2048)
+and the true-size run on the device draw from the SAME input family — element
+(r, c) depends only on (seed, m, r, c).  `_gaussian_rows` is the host form
+used for proxies; tests pin it against the device kernel and the oracle.
 """
 
 from __future__ import annotations
@@ -74,16 +76,53 @@ def make_matrix(cfg: int, b: int | None = None) -> np.ndarray:
     if kind == "spd":
         return _spd(rng(seed).standard_normal((m, m)))
     if kind == "randn_shift_blockwise":
-        k, bb = c["k"], c["b"]
         a = np.empty((m, m))
-        streams = np.random.SeedSequence(seed).spawn(k * k)
-        for i in range(k):
-            for j in range(k):
-                g = np.random.Generator(np.random.PCG64(streams[i * k + j]))
-                a[i * bb:(i + 1) * bb, j * bb:(j + 1) * bb] = g.standard_normal((bb, bb))
-        a[np.diag_indices(m)] += m
+        step = max(1, (1 << 22) // m)
+        for r0 in range(0, m, step):
+            a[r0:r0 + step] = _gaussian_rows(m, seed, float(m), r0, min(step, m - r0))
         return a
     raise ValueError(kind)
+
+
+_PH_M = (0xD2E7470EE14C6C93, 0xCA5A826395121157)
+_PH_W = (0x9E3779B97F4A7C15, 0xBB67AE8584CAA73B)
+
+
+def _mulhilo(a: int, x: np.ndarray):
+    lo32 = np.uint64(0xFFFFFFFF)
+    s32 = np.uint64(32)
+    al, ah = np.uint64(a & 0xFFFFFFFF), np.uint64(a >> 32)
+    xl, xh = x & lo32, x >> s32
+    p0, p1, p2, p3 = al * xl, al * xh, ah * xl, ah * xh
+    mid = (p0 >> s32) + (p1 & lo32) + (p2 & lo32)
+    return p3 + (p1 >> s32) + (p2 >> s32) + (mid >> s32), (mid << s32) | (p0 & lo32)
+
+
+def _gaussian_rows(m: int, seed: int, shift: float, r0: int, rows: int) -> np.ndarray:
+    """Rows [r0, r0+rows) of M = G + shift*I, G(r, c) = Box-Muller of Philox4x64-10 (key = seed)
+    at counter (r*m + c) >> 2: words 2q, 2q+1 (q = bit 1 of r*m + c) give u1 = ((w>>11)+1)/2^53,
+    u2 = (w>>11)/2^53, then sqrt(-2 ln u1) * (sin if bit 0 else cos)(2 pi u2)."""
+    e = (np.arange(r0, r0 + rows, dtype=np.uint64)[:, None] * np.uint64(m)
+         + np.arange(m, dtype=np.uint64)[None, :]).ravel()
+    ctr = [e >> np.uint64(2), np.zeros_like(e), np.zeros_like(e), np.zeros_like(e)]
+    k0, k1 = seed & 0xFFFFFFFFFFFFFFFF, 0
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            h0, l0 = _mulhilo(_PH_M[0], ctr[0])
+            h1, l1 = _mulhilo(_PH_M[1], ctr[2])
+            ctr = [h1 ^ ctr[1] ^ np.uint64(k0), l1, h0 ^ ctr[3] ^ np.uint64(k1), l0]
+            k0 = (k0 + _PH_W[0]) & 0xFFFFFFFFFFFFFFFF
+            k1 = (k1 + _PH_W[1]) & 0xFFFFFFFFFFFFFFFF
+    hiq = ((e >> np.uint64(1)) & np.uint64(1)).astype(bool)
+    wa = np.where(hiq, ctr[2], ctr[0])
+    wb = np.where(hiq, ctr[3], ctr[1])
+    u1 = ((wa >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+    u2 = (wb >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    rho, th = np.sqrt(-2.0 * np.log(u1)), 6.283185307179586 * u2
+    g = (rho * np.where((e & np.uint64(1)) == 1, np.sin(th), np.cos(th))).reshape(rows, m)
+    idx = np.arange(rows)
+    g[idx, r0 + idx] += shift
+    return g
 
 
 def node_flops(b: int) -> float:

@@ -61,3 +61,8 @@ def oracle_with_floor(a, k, targets, seed=123):
     moved = orc.invert_full(pert, k, memo=True, targets=list(targets))
     floor = {t: rel_err(moved[t], base[t]) for t in targets}
     return base, floor
+
+
+# the reference's own suite (tests/reference_suite/vendored) runs through its import shim in a
+# subprocess (tests/test_reference_suite.py); it is never collected into this session
+collect_ignore_glob = ["reference_suite/*"]

@@ -155,27 +155,6 @@ def test_config2_full_size(bri):
     assert _rel(out, x_col) <= 1e-9
 
 
-@pytest.mark.skipif(os.environ.get("BRI_SLOW") != "1", reason="config 4 at full size: ~90 s (set BRI_SLOW=1)")
-def test_config4_singular_pivot_matches_reference():
-    """BASELINE config 4 at true size (k=16, b=2048, SPD seed 3, block row 1): the reference stops
-    with SingularPivotError at branch A/D/A/D, block (2, 2) — a near-threshold
-    pivot test, so it also guards the accumulation order of the kernels."""
-    import torch
-
-    import paper_1612_00001_b200 as bri
-    from paper_1612_00001_b200 import workloads
-
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    cfg = workloads.config(4)
-    a = torch.from_numpy(workloads.make_matrix(4)).cuda()
-    prov = bri.make_memory_provider(a, cfg["k"])
-    with pytest.raises(bri.SingularPivotError) as exc:
-        bri.invert_blocks(prov, cfg["targets"])
-    assert "/".join(q.name for q in exc.value.path) == "A/D/A/D"
-    assert tuple(exc.value.pivot_block) == (2, 2)
-
-
 def test_bounded_arena_groups_targets():
     """A DAG that does not fit the arena budget is split into target groups
     (engine._run_grouped); results equal the unbounded run bit for bit, the
