@@ -84,6 +84,15 @@ int bri_level_batch(bri_arena* arena, void* stream, int nf, const int* fitems, i
                     const int* gitems, int* fstatus);
 
 /*
+ * bri_level_batch whose operands may still be in flight (the first DAG level of
+ * a run fed from pinned host memory): the caller's stream must already wait for
+ * the pivots; the solves wait on ev_l (cudaEvent_t, l operands landed) and the
+ * GEMM-subtracts on ev_rtr (rt and r landed).  Either event may be NULL.
+ */
+int bri_level_batch_gated(bri_arena* arena, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr);
+
+/*
  * Block inverses, batched — replaces core.py:238-263 (invert_dense).
  * items: 3 ints per block: slots (in, f, out); f is scratch; in is not modified.
  * status (device, count ints): pivot test of in.

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 
 from .errors import BadPartitionError
 
-__all__ = ["low_footprint_order", "Plan", "plan", "best_plan", "peak_live", "slots_used"]
+__all__ = ["low_footprint_order", "Plan", "plan", "plan_rank", "best_plan", "peak_live", "slots_used"]
 
 # op kinds of a plan
 LOAD = "load"        # ("load", (i, j), slot): base block M_ij from the source
@@ -40,6 +40,8 @@ INVERT = "invert"    # ("invert", t, (root_slot, f, out)): final inversion of ro
 OUTPUT = "output"    # ("output", t, slot): root t's (un-inverted) value is the result
 FREE = "free"        # ("free", slot): slot returns to the free list (no copy)
 HFREE = "hfree"      # ("hfree", hbuf): host buffer no longer needed
+SEND = "send"        # ("send", nid, slot, dst rank): node-sharded runs, value -> another rank
+RECV = "recv"        # ("recv", nid, slot, src rank): a value from another rank lands in slot
 
 
 def _consumers(sched):
@@ -120,6 +122,7 @@ class Plan:
     spills: int = 0           # device -> host copies
     reloads: int = 0          # host -> device copies
     loads: int = 0            # base-block loads from the source
+    transfers: int = 0        # node-sharded plans: sends + receives
     peak_slots: int = 0
     order: list = field(default_factory=list)
 
@@ -133,26 +136,68 @@ def plan(sched, nslots: int, max_host: int | None = None, invert_roots: bool = T
     Raises BadPartitionError when nslots < 7 or more than `max_host` host
     buffers would be needed.
     """
-    need = 7
-    if nslots < need:
-        raise BadPartitionError(f"a bounded DAG run needs at least {need} device blocks, the budget holds {nslots}")
     # a plan never holds more than every value and base block at once
-    nslots = min(nslots, len(sched.nodes) + len(sched.m_blocks_used()) + 8)
+    if nslots >= 7:
+        nslots = min(nslots, len(sched.nodes) + len(sched.m_blocks_used()) + 8)
     if order is None:
         order = low_footprint_order(sched)
     root_of = {}
     for t, nid in enumerate(sched.roots):
         root_of.setdefault(nid, []).append(t)
-
     # the access sequence: one step per node (its operands), then per root inversion
     steps = []
     for nid in order:
-        refs = []
-        for r in sched.nodes[nid].operands:
-            refs.append(("m", r[1], r[2]) if r[0] == "m" else ("v", r[1]))
-        steps.append(("node", nid, refs))
+        steps.append(("node", nid, _refs(sched, nid)))
         for t in root_of.get(nid, ()):
             steps.append(("invert" if invert_roots else "output", t, [("v", nid)]))
+    return _plan_steps(steps, nslots, max_host, keep_host, order)
+
+
+def _refs(sched, nid):
+    return [("m", r[1], r[2]) if r[0] == "m" else ("v", r[1]) for r in sched.nodes[nid].operands]
+
+
+def plan_rank(sched, owner: dict, rank: int, nslots: int, max_host: int | None = None,
+              invert_roots: bool = True, order: list | None = None) -> Plan:
+    """Bounded-footprint plan of ONE rank of a node-sharded run (distributed.run_sharded_bounded).
+
+    The job's step list is level-synchronous and identical on every rank: for each DAG level,
+    first the level's operand transfers in `distributed.level_transfers` order (a SEND reads a
+    value this rank owns or holds, a RECV lands a value from another rank in a fresh slot),
+    then this rank's own nodes of the level (in `order`, default the low-footprint order), each
+    root inverted right after it is produced.  The same Belady eviction as `plan` keeps the
+    rank within `nslots` device slots, spilling values — own or received — to pinned host
+    buffers.  Every rank posts its transfers in one global order, so blocking point-to-point
+    transfers cannot deadlock (the earliest unfinished transfer always has both ends posted).
+    """
+    from .distributed import level_transfers
+
+    if order is None:
+        order = low_footprint_order(sched)
+    rank_pos = {nid: i for i, nid in enumerate(order)}
+    root_of = {}
+    for t, nid in enumerate(sched.roots):
+        root_of.setdefault(nid, []).append(t)
+    steps = []
+    for n, ids in sched.levels().items():
+        for src, dst, nid in level_transfers(sched, owner, ids):
+            if src == rank:
+                steps.append(("send", (nid, dst), [("v", nid)]))
+            elif dst == rank:
+                steps.append(("recv", (nid, src), []))
+        for nid in sorted((i for i in ids if owner[i] == rank), key=rank_pos.__getitem__):
+            steps.append(("node", nid, _refs(sched, nid)))
+            for t in root_of.get(nid, ()):
+                steps.append(("invert" if invert_roots else "output", t, [("v", nid)]))
+    mine = [nid for nid in order if owner[nid] == rank]
+    return _plan_steps(steps, nslots, max_host, True, mine)
+
+
+def _plan_steps(steps, nslots: int, max_host, keep_host: bool, order) -> Plan:
+    """Belady slot assignment over an access sequence (see `plan`)."""
+    need = 7
+    if nslots < need:
+        raise BadPartitionError(f"a bounded DAG run needs at least {need} device blocks, the budget holds {nslots}")
     # next-use positions for Belady, per entity
     uses: dict = {}
     for pos, (_, _, refs) in enumerate(steps):
@@ -243,6 +288,7 @@ def plan(sched, nslots: int, max_host: int | None = None, invert_roots: bool = T
                         hfree.append(hb)
                 where[e] = s
             slots.append(where[e])
+        produced = None
         if kind == "node":
             fresh = [take(pos, pinned) for _ in range(3)]
             ops.append((NODE, ident, tuple(slots) + tuple(fresh)))
@@ -250,7 +296,19 @@ def plan(sched, nslots: int, max_host: int | None = None, invert_roots: bool = T
             ops.append((FREE, f))
             ops.append((FREE, w))
             free += [w, f]
+            produced = ident
             where[("v", ident)] = o
+        elif kind == "recv":
+            nid, peer = ident
+            o = take(pos, pinned)
+            ops.append((RECV, nid, o, peer))
+            out.transfers += 1
+            produced = nid
+            where[("v", nid)] = o
+        elif kind == "send":
+            nid, peer = ident
+            ops.append((SEND, nid, slots[0], peer))
+            out.transfers += 1
         elif kind == "output":
             ops.append((OUTPUT, ident, slots[0]))
         else:
@@ -262,8 +320,8 @@ def plan(sched, nslots: int, max_host: int | None = None, invert_roots: bool = T
         for e in set(refs):
             if e in where:
                 retire(e, pos)
-        if kind == "node":
-            e = ("v", ident)
+        if produced is not None:
+            e = ("v", produced)
             if next_use(e, pos + 1) is None:
                 retire(e, pos)
         out.peak_slots = max(out.peak_slots, nslots - len(free))
@@ -303,7 +361,7 @@ def slots_used(p: Plan) -> int:
     top = -1
     for op in p.ops:
         kind = op[0]
-        if kind in (LOAD, SPILL, RELOAD):
+        if kind in (LOAD, SPILL, RELOAD, SEND, RECV):
             top = max(top, op[2])
         elif kind in (NODE, INVERT):
             top = max(top, *op[2])

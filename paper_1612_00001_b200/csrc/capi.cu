@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX: free unless a profiler is attached
+
 #include "../../include/bri_b200.h"
 #include "bri_common.cuh"
 #include "bri_internal.h"
@@ -716,6 +718,14 @@ __global__ void fp64_peak_kernel(double* sink, int iters) {
 
 }  // namespace
 
+// NVTX range per C-ABI hot call (SURVEY §5 tracing): nsys / ncu --nvtx see the
+// level structure (schur / level batches, inversions, factorizations) directly.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define BRI_NVTX(name) NvtxScope bri_nvtx_scope_(name)
+
 // ==================================================================== C ABI
 extern "C" {
 
@@ -831,6 +841,7 @@ void bri_arena_destroy(bri_arena* arena) { delete arena; }
 
 int bri_gemm(bri_arena* ar, void* stream, int count, const int* items, int M, int N, int K, int a_r0,
              int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta) {
+  BRI_NVTX("bri_gemm");
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_gemm: bad arguments");
   if (((a_r0 | b_r0) & 1) != 0)
     return fail_msg("bri_gemm: a_r0 and b_r0 must be even (TMA boxes start on 16-byte boundaries)");
@@ -872,6 +883,7 @@ int bri_transpose(bri_arena* ar, void* stream, int count, const int* items) {
 
 int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, int* ipiv, int* perm,
                     int* status) {
+  BRI_NVTX("bri_getrf_batch");
   if (ar == nullptr || slots == nullptr || count < 0) return fail_msg("bri_getrf_batch: bad arguments");
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -895,6 +907,7 @@ int bri_getrf_batch(bri_arena* ar, void* stream, int count, const int* slots, in
 }
 
 int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, const int* perm) {
+  BRI_NVTX("bri_getrs_batch");
   if (ar == nullptr || items == nullptr || perm == nullptr || count < 0)
     return fail_msg("bri_getrs_batch: bad arguments");
   if (count == 0) return 0;
@@ -917,6 +930,7 @@ int bri_getrs_batch(bri_arena* ar, void* stream, int count, const int* items, co
 }
 
 int bri_invert_batch(bri_arena* ar, void* stream, int count, const int* items, int* status) {
+  BRI_NVTX("bri_invert_batch");
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_invert_batch: bad arguments");
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1004,6 +1018,7 @@ int bri_schur_batch(bri_arena* ar, void* stream, int count, const int* items, in
 
 int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* items, int* status, void* ev_l,
                           void* ev_rtr) {
+  BRI_NVTX("bri_schur_batch_gated");
   if (ar == nullptr || items == nullptr || count < 0) return fail_msg("bri_schur_batch: bad arguments");
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1138,8 +1153,21 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
 // every node only pays its own fused GEMM-subtract.  Same kernels, same
 // operand bytes: each W and out is bit-identical to bri_schur_batch's large-
 // batch (unfolded) path.
+int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr);
+
 int bri_level_batch(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems, int ng,
                     const int* gitems, int* fstatus) {
+  return bri_level_batch_gated(ar, stream, nf, fitems, ns, sitems, ng, gitems, fstatus, nullptr, nullptr);
+}
+
+// ev_l / ev_rtr (optional): the l operands / the rt and r operands are still
+// being copied in (first level of a run from pinned host memory); the solves
+// wait on ev_l, the GEMM-subtracts on ev_rtr, through external event nodes of
+// the captured graph (the caller re-records the same persistent events).
+int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr) {
+  BRI_NVTX("bri_level_batch");
   if (ar == nullptr || nf < 0 || ns < 0 || ng < 0 || (nf && !fitems) || (ns && !sitems) || (ng && !gitems))
     return fail_msg("bri_level_batch: bad arguments");
   if (nf == 0 && ns == 0 && ng == 0) return 0;
@@ -1188,15 +1216,20 @@ int bri_level_batch(bri_arena* ar, void* stream, int nf, const int* fitems, int 
       if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, nf, L, sc)) return rc;
     }
     if (ns > 0) {   // W = U^-1 L^-1 P l with the permutation of the solve's factor
+      if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
       BRI_CHECK(launch_permcopy(ar->v, d_lw, ns, sc.pi, n, false, st, d_fidx));
       if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false)) return rc;
     }
+    if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
+    if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
     if (ng > 0) return gemm_call(ar, st, d_g, ng, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
     return 0;
   };
   std::vector<uintptr_t> key = graph_key(2, ar, ng, dev);
   key.push_back((uintptr_t)nf);
   key.push_back((uintptr_t)ns);
+  key.push_back((uintptr_t)ev_l);
+  key.push_back((uintptr_t)ev_rtr);
   if (int rc = run_graphed(ar->ctx, s, key, issue)) return rc;
   if (fstatus && nf > 0)
     BRI_CHECK(cudaMemcpyAsync(fstatus, sc.status, (size_t)nf * 4, cudaMemcpyDeviceToDevice, s));
@@ -1205,6 +1238,7 @@ int bri_level_batch(bri_arena* ar, void* stream, int nf, const int* fitems, int 
 
 int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ldm, int count,
                       const int* items) {
+  BRI_NVTX("bri_gather_blocks");
   if (ar == nullptr || M == nullptr || items == nullptr || count < 0) return fail_msg("bri_gather_blocks: bad arguments");
   if (count == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1236,6 +1270,7 @@ int bri_gather_elements(bri_arena* ar, void* stream, const double* M, long long 
 
 int bri_load_host_blocks(bri_arena* ar, void* stream, const double* host, long long ldh, int count,
                          const int* items) {
+  BRI_NVTX("bri_load_host_blocks");
   if (ar == nullptr || host == nullptr || items == nullptr || count < 0 || ldh < ar->v.n)
     return fail_msg("bri_load_host_blocks: bad arguments");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1253,6 +1288,7 @@ int bri_load_host_blocks(bri_arena* ar, void* stream, const double* host, long l
 
 int bri_rbf_blocks(bri_arena* ar, void* stream, const double* x, int n, int d, double denom, double ridge,
                    const int* rmap, const int* cmap, int count, const int* items) {
+  BRI_NVTX("bri_rbf_blocks");
   if (ar == nullptr || x == nullptr || items == nullptr || n < 1 || d < 1 || count < 0 ||
       (rmap == nullptr) != (cmap == nullptr))
     return fail_msg("bri_rbf_blocks: bad arguments");
@@ -1277,6 +1313,7 @@ int bri_rbf_dense(void* stream, const double* x, int n, int d, double denom, dou
 
 int bri_randn_blocks(bri_arena* ar, void* stream, long long m, unsigned long long seed, double shift,
                      const int* rmap, const int* cmap, int count, const int* items) {
+  BRI_NVTX("bri_randn_blocks");
   if (ar == nullptr || items == nullptr || m < 1 || count < 0 || (rmap == nullptr) != (cmap == nullptr))
     return fail_msg("bri_randn_blocks: bad arguments");
   if (count == 0) return 0;

@@ -819,7 +819,13 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   // (one row per thread on a 16-CTA cluster is faster alone at 4096 rows — 1.70
   // vs 1.87 us/column — but a 16-SM cluster waits for SMs next to the
   // concurrent trailing update: config 2 went from 35.0 to 39.4 ms)
-  if (h > max_panel_rows()) {
+  // BRI_TALL_ROWS lowers the tall-panel threshold (tests and compute-sanitizer runs
+  // exercise the tall kernel on small matrices); default: what registers cannot hold
+  static const int tall_rows = [] {
+    const char* e = getenv("BRI_TALL_ROWS");
+    return e ? atoi(e) : max_panel_rows();
+  }();
+  if (h > tall_rows) {
     TallArgs t{a, slots, j0, nb, pidx, sc.ipiv, sc.sigma, sc.pairs, sc.orig, n_stride, pair_stride};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(count * TALL_CS);

@@ -20,7 +20,8 @@ A single target cannot be split this way: every rank then runs a replica.
 
 from __future__ import annotations
 
-__all__ = ["shard_targets", "gather_blocks", "assign_owners", "level_transfers", "exchange", "run_sharded"]
+__all__ = ["shard_targets", "gather_blocks", "assign_owners", "level_transfers", "exchange", "run_sharded",
+           "run_sharded_bounded", "rank_peak_blocks"]
 
 
 def shard_targets(targets, rank: int, world: int):
@@ -214,3 +215,88 @@ def rank_peak_blocks(sched, owner: dict, rank: int, scratch: int = 2) -> int:
         prev_own = sum(1 for nid in mine if nid not in roots)
         held_roots += sum(1 for nid in mine if nid in roots)
     return max(peak, held_roots + 2)
+
+
+# --------------------------------------------------------------------------
+# Node sharding within a per-rank memory bound (config 5 on 2 / 4 / 8 GPUs)
+# --------------------------------------------------------------------------
+
+def run_sharded_bounded(sched, rank: int, world: int, ex, plan, invert_roots: bool = True, group=None):
+    """Replay one rank's bounded plan (bounded.plan_rank) of a node-sharded run.
+
+    Every node still runs exactly once in the job, on its owner; each rank keeps at most
+    plan.nslots device blocks, spilling values (own or received) to pinned host buffers;
+    operand values move between ranks by point-to-point transfers posted in the job's one
+    global order (no deadlock, see plan_rank).  Executor `ex` (device: engine._BoundedExecutor,
+    CPU tests: an oracle executor):
+
+      ex.claim(slot) / ex.release(slot)      slot bookkeeping
+      ex.slot(slot) -> tensor                the block buffer (P2P source / destination)
+      ex.load(slot, (i, j))                  base block M_ij (1-based) into slot
+      ex.node(nid, slots)                    (p, rt, l, r, out, f, w) Schur node
+      ex.invert(t, (root, f, out)) -> tensor final inversion of root t (result tensor)
+      ex.output(t, slot) -> tensor           root value as the result (invert_roots=False)
+      ex.spill(slot, hbuf) / ex.reload(slot, hbuf)
+      ex.statuses(nids) -> {nid: int}; ex.root_status(t) -> int
+      ex.empty_result() -> tensor            receive buffer for a root result on rank 0
+    Returns ({target: tensor} on rank 0 else None, node statuses, root statuses) — the statuses
+    all-reduced so that every rank raises the reference's error."""
+    import torch
+    import torch.distributed as dist
+
+    from . import bounded as bd
+
+    if world > 1:
+        dist.barrier(group=group)
+    results, mine_roots = {}, []
+    for op in plan.ops:
+        kind = op[0]
+        if kind == bd.NODE:
+            for s in op[2][4:]:
+                ex.claim(s)
+            ex.node(op[1], op[2])
+        elif kind == bd.FREE:
+            ex.release(op[1])
+        elif kind == bd.LOAD:
+            ex.claim(op[2])
+            ex.load(op[2], op[1])
+        elif kind == bd.SPILL:
+            ex.spill(op[2], op[3])
+        elif kind == bd.RELOAD:
+            ex.claim(op[2])
+            ex.reload(op[2], op[3])
+        elif kind == bd.SEND:
+            dist.send(ex.slot(op[2]), op[3], group=group)
+        elif kind == bd.RECV:
+            ex.claim(op[2])
+            dist.recv(ex.slot(op[2]), op[3], group=group)
+        elif kind == bd.INVERT:
+            t, (r, f, o) = op[1], op[2]
+            ex.claim(f)
+            ex.claim(o)
+            results[t] = ex.invert(t, (r, f, o))
+            mine_roots.append(t)
+        elif kind == bd.OUTPUT:
+            results[op[1]] = ex.output(op[1], op[2])
+            mine_roots.append(op[1])
+    owner = assign_owners(sched, world)
+    st = ex.statuses([nid for nid in owner if owner[nid] == rank])
+    nn = len(sched.nodes)
+    flat = torch.zeros(nn + len(sched.roots), dtype=torch.int64, device=ex.device)
+    for nid, v in st.items():
+        flat[nid] = int(v)
+    if invert_roots:
+        for t in mine_roots:
+            flat[nn + t] = int(ex.root_status(t))
+    if world > 1:
+        dist.all_reduce(flat, group=group)
+    # root results to rank 0, in target order (a global order again)
+    for t, nid in enumerate(sched.roots):
+        o = owner[nid]
+        if o == rank and rank != 0:
+            dist.send(results[t].contiguous(), 0, group=group)
+        elif o != rank and rank == 0:
+            results[t] = ex.empty_result()
+            dist.recv(results[t], o, group=group)
+    host = flat.cpu().numpy()
+    return (results if rank == 0 else None), host[:nn], host[nn:]

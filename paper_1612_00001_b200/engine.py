@@ -31,6 +31,7 @@ reduction raises SingularBlockError (core.py:252-254).
 
 from __future__ import annotations
 
+import os
 import threading
 import time
 from collections import OrderedDict
@@ -298,7 +299,7 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                 part = ids[c0:c0 + chunk]
                 slot_of = lambda r: mslot[(r[1], r[2])] if r[0] == "m" else val[r[1]]
                 scratch = []
-                if b > SMALL_MAX and gates is None and len(part) > 2:
+                if b > SMALL_MAX and len(part) > 2:
                     # shared work: one factorization per distinct pivot, one solve per
                     # distinct (pivot, l), one fused GEMM-subtract per node
                     fidx, sidx, fitems, sitems, gitems = {}, {}, [], [], []
@@ -319,7 +320,11 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                         gitems.append((slot_of(refs[1]), sidx[sk], slot_of(refs[3]), out))
                         val[nid] = out
                         pos[nid] = pbase + fidx[refs[0]]
-                    arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)])
+                    if gates is not None:   # first level from pinned host: l, rt, r may be in flight
+                        arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)], *gates)
+                        gates = None
+                    else:
+                        arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)])
                     pbase += len(fitems)
                     info.factorizations += len(fitems)
                     info.solves += len(sitems)
@@ -631,6 +636,63 @@ class _ArenaExecutor:
         return torch.empty((self.b, self.b), dtype=torch.float64, device=self.device)
 
 
+class _BoundedExecutor:
+    """Device executor of distributed.run_sharded_bounded: a fixed arena (the rank's plan
+    slots) plus pinned host buffers for spilled values; every copy and P2P transfer is
+    ordered on the run's stream, exactly like the one-GPU bounded run (_run_bounded)."""
+
+    def __init__(self, arena: Arena, src, device: int, nnodes: int, hbufs):
+        torch = _torch()
+        self.arena, self.src, self.b, self.hbufs = arena, src, src.b, hbufs
+        self.device = f"cuda:{device}"
+        self.st = torch.zeros(max(1, nnodes), dtype=torch.int32, device=self.device)
+        self.rst = {}
+        self.nodes_run = 0
+
+    def claim(self, s):
+        self.arena.claim(s)
+
+    def release(self, s):
+        self.arena.release(s)
+
+    def slot(self, s):
+        return self.arena.tensor[s]
+
+    def load(self, s, ij):
+        self.src.load(self.arena, [(ij[0], ij[1], s)])
+
+    def node(self, nid, slots):
+        self.arena.schur([slots], self.st[nid:nid + 1])
+        self.nodes_run += 1
+
+    def invert(self, t, slots):
+        torch = _torch()
+        st = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.arena.invert([slots], st)
+        self.rst[t] = st
+        return self.arena.view(slots[2]).clone()
+
+    def output(self, t, s):
+        return self.arena.view(s)[:, : self.b].clone()
+
+    def spill(self, s, hb):
+        self.hbufs[hb].copy_(self.arena.tensor[s], non_blocking=True)
+
+    def reload(self, s, hb):
+        self.arena.tensor[s].copy_(self.hbufs[hb], non_blocking=True)
+
+    def statuses(self, nids):
+        host = self.st.cpu().numpy()
+        return {nid: int(host[nid]) for nid in nids}
+
+    def root_status(self, t):
+        return int(self.rst[t].item())
+
+    def empty_result(self):
+        torch = _torch()
+        return torch.empty((self.b, self.b), dtype=torch.float64, device=self.device)
+
+
 def invert_blocks_sharded(provider: BlockProvider, targets, ws: Workspace | None = None, group=None):
     """Blocks `targets` of M^-1 over all ranks of the process group (one per GPU): ONE
     deduplicated DAG over every target, each level's nodes dealt to ranks with operand
@@ -660,8 +722,15 @@ def invert_blocks_sharded(provider: BlockProvider, targets, ws: Workspace | None
     sched = _schedule(key, k, specs, None)
     owner = assign_owners(sched, world)
     need = rank_peak_blocks(sched, owner, rank)
-    if need > _budget_slots(ws, src.b, device):
-        raise BadPartitionError(f"rank {rank} needs {need} blocks of order {src.b}; raise the budget or the rank count")
+    budget = _budget_slots(ws, src.b, device)
+    # every rank decides the same way (the plans must agree on the transfer sequence)
+    import torch
+
+    flag = torch.tensor([1 if need > budget or ws.schedule == "bounded" else 0], device=f"cuda:{device}")
+    if world > 1:
+        dist.all_reduce(flag, group=group)
+    if int(flag.item()):
+        return _sharded_bounded(src, sched, owner, rank, world, ws, device, budget, targets, group)
     arena = cached_arena(src.b, need, device, gauge=ws.gauge)
     ex = _ArenaExecutor(arena, src, device, len(sched.nodes))
     try:
@@ -674,6 +743,38 @@ def invert_blocks_sharded(provider: BlockProvider, targets, ws: Workspace | None
     ws.executed.add_nodes(ex.nodes_run, targets=sum(1 for nid in sched.roots if owner[nid] == rank))
     info = RunInfo("sharded", len(targets), len(sched.nodes), sum(sched.tree_nodes(t) for t in range(len(targets))),
                    {n: len(v) for n, v in sched.levels().items()}, need, 0, ws.gauge.peak_blocks)
+    out = [res[t] for t in range(len(targets))] if res is not None else None
+    return out, info
+
+
+def _sharded_bounded(src, sched, owner, rank, world, ws, device, budget, targets, group):
+    """invert_blocks_sharded when a rank's level-by-level footprint exceeds its budget (config 5
+    on 2 / 4 / 8 GPUs): each rank replays its own bounded plan (bounded.plan_rank) — its nodes of
+    each level in a low-footprint order within `budget` slots, spilled values in pinned host
+    buffers (the host budget is shared by the ranks of one node), operand values exchanged
+    point to point in the job's global order (distributed.run_sharded_bounded)."""
+    from . import bounded as bd
+    from .distributed import run_sharded_bounded
+
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    max_host = max(0, _host_slots(ws, src.b, device) // max(1, local))
+    p = bd.plan_rank(sched, owner, rank, budget, max_host=max_host)
+    nslots = bd.slots_used(p)
+    arena = cached_arena(src.b, nslots, device, gauge=ws.gauge)
+    hbufs = _pinned_pool(device, src.b, arena.ld, p.host_buffers)
+    ex = _BoundedExecutor(arena, src, device, len(sched.nodes), hbufs)
+    try:
+        res, pstat, rstat = run_sharded_bounded(sched, rank, world, ex, p, group=group)
+    finally:
+        arena.release_all()
+    sched.first_failure(pstat, rstat, src.b)
+    for t in range(len(sched.specs)):
+        ws.counters.add_nodes(sched.tree_nodes(t), targets=1)
+    ws.executed.add_nodes(ex.nodes_run, targets=sum(1 for nid in sched.roots if owner[nid] == rank))
+    info = RunInfo("sharded-bounded", len(targets), len(sched.nodes),
+                   sum(sched.tree_nodes(t) for t in range(len(targets))),
+                   {n: len(v) for n, v in sched.levels().items()}, nslots, 1, ws.gauge.peak_blocks,
+                   spills=p.spills, reloads=p.reloads, host_blocks=p.host_buffers)
     out = [res[t] for t in range(len(targets))] if res is not None else None
     return out, info
 

@@ -265,6 +265,13 @@ def test_node_sharded_device_executor_world1(bri, golden):
         for x, y in zip(got, want):
             assert torch.equal(x, y)
         assert ws.gauge.live_blocks == 0
+        # the per-rank bounded plan (config 5 on N GPUs): 9 device blocks, spills to pinned host
+        wsb = bri.Workspace(schedule="bounded", arena_bytes=9 * 128 * 128 * 8)
+        got_b, info_b = bri.invert_blocks_sharded(prov, targets, wsb)
+        assert info_b.schedule == "sharded-bounded" and info_b.spills > 0 and info_b.arena_slots <= 9, info_b
+        for x, y in zip(got_b, want):
+            assert torch.equal(x, y)
+        assert wsb.gauge.live_blocks == 0
         data, meta = golden
         with pytest.raises(bri.SingularPivotError) as exc:
             bri.invert_blocks_sharded(bri.make_memory_provider(data["singular_matrix"], 3), [(1, 1)])

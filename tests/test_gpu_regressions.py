@@ -54,3 +54,13 @@ def test_tall_panel_heavy_pivoting_node(cuda_dev):
     res = _probe(["--n", "10240", "--repeats", "3", "--node"], {"BRI_CAP_ROWS": "1000000"})
     assert res["identical"], res
     assert max(res["resid"]) <= 1e-6, res
+
+
+def test_tall_kernel_small_heavy_pivoting(cuda_dev):
+    """The tall-panel kernel forced onto small panels (BRI_TALL_ROWS=256): a plain Gaussian
+    n = 1536 dense inverse — interchanges in nearly every column, 16-CTA clusters with only
+    ~100 rows each — repeated with and without concurrent GEMMs: bit-identical, tight residual.
+    The same configuration is what the compute-sanitizer runs use (profiles/r02_sanitizer_*)."""
+    res = _probe(["--n", "1536", "--repeats", "4"], {"BRI_TALL_ROWS": "256"})
+    assert res["identical"], res
+    assert max(res["resid"]) <= 1e-10, res
