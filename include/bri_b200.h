@@ -194,6 +194,16 @@ int bri_randn_window(void* stream, long long m, unsigned long long seed, double 
                      long long col0, int rows, int cols, double* out, long long ldo);
 
 /*
+ * Device -> host store of a result block — the output side of sink.put
+ * (formats.py:249-282): one 2-D async copy of rows x cols doubles from a
+ * row-major device buffer (leading dim ldd) into a row-major host canvas
+ * (leading dim ldh).  With a pinned canvas the copy is asynchronous on
+ * `stream`; the caller synchronizes before reading the canvas.
+ */
+int bri_store_host(void* stream, double* host, long long ldh, const double* dev, long long ldd, int rows,
+                   int cols);
+
+/*
  * Host -> device block loads — the fetch of providers.py:318-336 for a matrix in
  * (pinned) host memory: one 2-D async copy per item (block row i, block col j,
  * slot), 0-based, from the row-major host matrix with leading dim ldh into the

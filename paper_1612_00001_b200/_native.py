@@ -49,6 +49,8 @@ SIGNATURES = [
     ("bri_schur_batch_gated", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_void_p, _c_void_p, _c_void_p]),
     ("bri_fp64_peak", _c_int, [_c_void_p, _c_int, ctypes.POINTER(_c_double)]),
     ("bri_level_batch", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT, _c_void_p]),
+    ("bri_store_host", _c_int, [_c_void_p, _c_void_p, ctypes.c_longlong, _c_void_p, ctypes.c_longlong, _c_int,
+                                _c_int]),
     ("bri_level_batch_gated", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT,
                                        _c_void_p, _c_void_p, _c_void_p]),
 ]

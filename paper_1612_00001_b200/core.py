@@ -20,6 +20,8 @@ does not call them (it batches whole DAG levels, engine.py).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .device import Arena, current_device
@@ -45,6 +47,9 @@ class Workspace:
     node once in a low-footprint order within the device budget, spilling
     node values to pinned host memory (bounded.py); "dag" switches to it by
     itself when one target's DAG does not fit.  All return the same values.
+    The default (schedule=None) is "dag", or the BRI_SCHEDULE environment variable:
+    the DAG run trades the reference's <= 2k+4 live-block contract
+    for evaluating every distinct node once; "tree" keeps the contract exactly.
     arena_bytes: device-memory budget of one run (default: 85% of free HBM).
     host_bytes: pinned host memory a bounded run may use for spilled values
     (default: 60% of the host's available memory).
@@ -53,8 +58,10 @@ class Workspace:
     __slots__ = ("counters", "gauge", "executed", "schedule", "arena_bytes", "host_bytes", "device")
 
     def __init__(self, counters: OpCounters | None = None, gauge: MemoryGauge | None = None, *,
-                 schedule: str = "dag", arena_bytes: int | None = None, host_bytes: int | None = None,
+                 schedule: str | None = None, arena_bytes: int | None = None, host_bytes: int | None = None,
                  device: int | None = None):
+        if schedule is None:   # process-wide default: BRI_SCHEDULE=tree keeps the reference's <= 2k+4 bound
+            schedule = os.environ.get("BRI_SCHEDULE", "dag")
         if schedule not in ("dag", "tree", "bounded"):
             raise ValueError(f"schedule must be 'dag', 'tree' or 'bounded', got {schedule!r}")
         self.counters = counters if counters is not None else OpCounters()

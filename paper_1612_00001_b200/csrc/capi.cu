@@ -277,8 +277,14 @@ struct LuFold {
   cudaEvent_t ev_rtr = nullptr;
 };
 
+// variant_count (default: count) picks the blocking variant (panel extension into
+// the next block, GEMM caps) — the variants round differently, so a DAG level
+// keeps the variant of its NODE count even when its distinct pivots are few
+// (bri_level_batch): results then do not depend on how much work is shared.
 int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int* dev_ffff, const int* dev_ff,
-                 int count, const LuLayout& L, const LuScratch& sc, const LuFold* fold = nullptr) {
+                 int count, const LuLayout& L, const LuScratch& sc, const LuFold* fold = nullptr,
+                 int variant_count = -1) {
+  const int vcount = variant_count >= 0 ? variant_count : count;
   const ArenaView& v = ar->v;
   const int n = v.n;
   bri_ctx* ctx = ar->ctx;
@@ -327,13 +333,13 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     const char* e = getenv("BRI_TRAIL_CAP");
     return e ? atoi(e) : -1;
   }();
-  const int trail_cap = trail_cap_env >= 0 ? trail_cap_env : (count <= 2 ? 80 : 0);
+  const int trail_cap = trail_cap_env >= 0 ? trail_cap_env : (vcount <= 2 ? 80 : 0);
 
   static const int fold_cap_env = [] {
     const char* e = getenv("BRI_FOLD_CAP");
     return e ? atoi(e) : -1;
   }();
-  const int fold_cap = fold_cap_env >= 0 ? fold_cap_env : (count <= 2 ? 48 : 0);
+  const int fold_cap = fold_cap_env >= 0 ? fold_cap_env : (vcount <= 2 ? 48 : 0);
   // The caps pay while the pivot chain is the critical path (n <= 4096); for
   // larger orders the bulk updates are, and every SM should take them:
   // measured on one node + inversion (tools/sweep_caps_large.sh), uncapped vs
@@ -416,7 +422,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     const char* e = getenv("BRI_LU_EXTEND");
     return e ? atoi(e) : -1;
   }();
-  const bool extend = lookahead && (extend_env >= 0 ? extend_env != 0 : count <= 2);
+  const bool extend = lookahead && (extend_env >= 0 ? extend_env != 0 : vcount <= 2);
   const int W0 = n < outer ? n : outer;
   const int ext0 = extend ? (n < 2 * outer ? n : 2 * outer) : W0;
   if (int rc = factor_block(0, W0, 0, ext0, nullptr)) return rc;
@@ -1213,7 +1219,7 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
   auto issue = [&](cudaStream_t st) -> int {
     if (nf > 0) {
       BRI_CHECK(launch_copy(ar->v, d_pf, nf, st));
-      if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, nf, L, sc)) return rc;
+      if (int rc = getrf_device(ar, st, d_f, d_ffff, d_ff, nf, L, sc, nullptr, ng > nf ? ng : nf)) return rc;
     }
     if (ns > 0) {   // W = U^-1 L^-1 P l with the permutation of the solve's factor
       if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
@@ -1265,6 +1271,16 @@ int bri_gather_elements(bri_arena* ar, void* stream, const double* M, long long 
   bri::count_launch();
   gather_elements_kernel<<<dim3(gx, count), 256, 0, s>>>(ar->v, M, ldm, m, rmap, cmap, dev);
   BRI_CHECK(cudaGetLastError());
+  return 0;
+}
+
+int bri_store_host(void* stream, double* host, long long ldh, const double* dev, long long ldd, int rows,
+                   int cols) {
+  if (host == nullptr || dev == nullptr || rows < 0 || cols < 0 || ldh < cols || ldd < cols)
+    return fail_msg("bri_store_host: bad arguments");
+  if (rows == 0 || cols == 0) return 0;
+  BRI_CHECK(cudaMemcpy2DAsync(host, (size_t)ldh * 8, dev, (size_t)ldd * 8, (size_t)cols * 8, rows,
+                              cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

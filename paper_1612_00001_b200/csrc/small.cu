@@ -1,16 +1,36 @@
 // K6: fused one-CTA Schur node / block inverse for small blocks (n <= 96), sm_100a.
 //
-// For b <= 96 a whole node of the reference's `_fold` (engine.py:157-180) fits
-// in one SM's shared memory: pivot LU with partial pivoting (dgetrf semantics
-// on the X-world view, core.py:249), the growth-scaled singularity test
-// (core.py:200-209), the solve W = P^-1 * l (dgetrs, core.py:259) and the
-// fused update out = r - rt * W run in one launch per DAG level, one CTA per
-// node.  This is the latency-bound regime of BASELINE config 1 (b = 64) and
-// of every small-b case in the reference's own test-suite.
+// For b <= 96 a whole node of the reference's `_fold` (engine.py:157-180) is
+// one CTA's work: the pivot solve W = P^-1 * l with partial pivoting (dgetrf
+// pivot decisions on the X-world view, core.py:249, and the growth-scaled
+// singularity test of core.py:200-209) and the fused update out = r - rt * W
+// on the tensor cores, in one launch per DAG level, one CTA per node.  This is
+// the latency-bound regime of BASELINE config 1 (b = 64) and of every small-b
+// case in the reference's own test suite.
 //
 // In X-world the node computes  out^ = r^ - rt^ * (p^)^-1 * l^  which is the
 // transpose of the reference's  r - l @ (inv(p) @ rt)  (all hats are the
 // column-major views of the row-major blocks).
+//
+// Design (latency first — a 64 x 64 node is ~0.7 MFLOP, nothing to stream):
+//  * The augmented matrix [p^ | l^] (N x 2N) lives in REGISTERS: lane owns rows
+//    lane + 32h, warp w owns columns w + NW q.  No smem traffic in the sweep.
+//  * One Gauss-Jordan sweep replaces LU + forward + backward substitution (three
+//    serial sweeps): step j eliminates column j from every other row, so after
+//    N steps the solution is the right half scaled by the pivots.  The rows below
+//    the diagonal see exactly dgetf2's updates (multiplier x * (1/pivot), then
+//    fma(-l, u, a)), so the pivot sequence and the U diagonal the singularity
+//    test reads are LU's; rows above are eliminated instead of back-substituted.
+//  * Interchanges move nothing: each row keeps its physical place and carries
+//    its LAPACK *position*; the argmax breaks ties on position (idamax's first
+//    index of the permuted column), and the position bookkeeping reproduces the
+//    swap of rows j and p.
+//  * One __syncthreads per column: warp (j mod NW) owns column j, finds the pivot
+//    (REDUX argmax), writes the multipliers of all rows to a double-buffered
+//    smem vector; every warp then broadcasts the pivot row by shuffles and
+//    updates its own columns right of j.
+//  * rt^ streams into smem by cp.async while the sweep runs; out = r - rt * W
+//    is DMMA (mma.sync m16n8k4 f64 -> SASS DMMA.8x8x4) from smem.
 #include <climits>
 
 #include "bri_common.cuh"
@@ -20,33 +40,38 @@ namespace bri {
 
 namespace {
 
-constexpr int SN_THREADS = 256;
+// warps per CTA: 8 up to N = 64 (the 64 x 128 augmented block is 32 doubles per lane);
+// 16 for N = 96 so that a lane's share (36 doubles) stays in registers
+template <int N>
+constexpr int sn_warps() { return N > 64 ? 16 : 8; }
 
-#ifdef BRI_SMALL_PROFILE
-__device__ unsigned long long g_small_phase[8];
-#define SPROF(k)                                                   \
-  do {                                                             \
-    if (threadIdx.x == 0 && blockIdx.x == 0) {                     \
-      const unsigned long long now = clock64();                    \
-      atomicAdd(&g_small_phase[k], now - t_last);                  \
-      t_last = now;                                                \
-    }                                                              \
-  } while (0)
-#else
-#define SPROF(k) do { } while (0)
-#endif
+BRI_DEVI void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+BRI_DEVI void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+BRI_DEVI void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-template <int NMAX>
-__global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, const int* items, int mode,
-                                                                int* status) {
-  constexpr int LDS = NMAX + 1;
-  constexpr int LDW = NMAX + 8;    // W rows: 8 columns x 4 rows per warp access hit 2 wavefronts
+template <int N>
+constexpr int sn_ldr() { return N + 8; }   // == 8 (mod 16) doubles: conflict-free DMMA fragment loads
+
+template <int N>
+constexpr int small_smem() { return 2 * N * sn_ldr<N>() * 8; }
+
+// mode 0: Schur node (items: p, rt, l, r, out);  mode 1: out = p^-1 (items: in, -, -, -, out)
+template <int N>
+__global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(ArenaView a, const int* items, int mode,
+                                                                         int* status) {
+  constexpr int NW = sn_warps<N>();
+  constexpr int SN_THREADS = 32 * NW;
+  constexpr int R = N / 32;        // rows per lane
+  constexpr int Q = 2 * N / NW;    // augmented columns per warp (N of p^, N of the right-hand side)
+  constexpr int LDR = sn_ldr<N>();
   extern __shared__ double sm[];
-  double* F = sm;                  // factor of p^   (F[c * LDS + i] = element (i, c))
-  double* RT = F + NMAX * LDS;     // rt^ (mode 0 only)
-  double* W = RT + NMAX * LDS;     // right-hand side / solution, row-major: W[i * LDW + c]
-  __shared__ int perm[NMAX];
-  __shared__ int piv_s;
+  double* RTs = sm;                // RTs[k * LDR + i] = rt^(i, k)
+  double* Ws = sm + N * LDR;       // Ws[k * LDR + c]  = W(k, c)
+  __shared__ double mult[2][N];
+  __shared__ double pvs[N];
+  __shared__ int prow_s[2], ppos_s[2];
   __shared__ unsigned long long scale_bits;
   __shared__ int first_bad;
 
@@ -55,192 +80,200 @@ __global__ void __launch_bounds__(SN_THREADS) small_node_kernel(ArenaView a, con
   const double* P = a.base + (long long)it[0] * a.slot_elems;
   const double* Rt = a.base + (long long)it[1] * a.slot_elems;
   const double* Lb = a.base + (long long)it[2] * a.slot_elems;
-  const double* R = a.base + (long long)it[3] * a.slot_elems;
+  const double* Rb = a.base + (long long)it[3] * a.slot_elems;
   double* Out = a.base + (long long)it[4] * a.slot_elems;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-#ifdef BRI_SMALL_PROFILE
-  unsigned long long t_last = clock64();
-#endif
   if (tid == 0) {
     scale_bits = 0ull;
     first_bad = INT_MAX;
   }
-  if (tid < n) perm[tid] = tid;
-  __syncthreads();
+  // rt^ -> smem, asynchronously (only the GEMM reads it); rows k >= n are zero
+  if (mode == 0) {
+    for (int e = tid; e < N * (N / 2); e += SN_THREADS) {
+      const int k = e / (N / 2), i2 = 2 * (e % (N / 2));
+      double* dst = RTs + k * LDR + i2;
+      if (k < n && i2 < n) cp_async16(dst, Rt + i2 + (long long)k * ld);
+      else dst[0] = dst[1] = 0.0;
+    }
+    cp_async_commit();
+    for (int e = tid; e < (N - n) * N; e += SN_THREADS) Ws[(n + e / N) * LDR + e % N] = 0.0;
+  }
+
+  // [p^ | l^] (or [p^ | I]) into registers; max |p| for the singularity test
+  double A[R][Q];
+  int pos[R];
   double mx = 0.0;
-  for (int e = tid; e < n * n; e += SN_THREADS) {
-    const int i = e % n, c = e / n;
-    const double v = P[i + (long long)c * ld];
-    F[c * LDS + i] = v;
-    const double av = fabs(v);
-    if (__double_as_longlong(av) > __double_as_longlong(mx)) mx = av;
-    if (mode == 0) RT[c * LDS + i] = Rt[i + (long long)c * ld];
+#pragma unroll
+  for (int h = 0; h < R; ++h) {
+    const int r = lane + 32 * h;
+    pos[h] = r;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int c = warp + NW * q;
+      double v = 0.0;
+      if (c < N) {
+        if (r < n && c < n) v = P[r + (long long)c * ld];
+        const double av = fabs(v);
+        if (__double_as_longlong(av) > __double_as_longlong(mx)) mx = av;   // NaN counts as largest
+      } else if (r < n && c - N < n) {
+        v = mode == 1 ? (r == c - N ? 1.0 : 0.0) : Lb[r + (long long)(c - N) * ld];
+      }
+      A[h][q] = v;
+    }
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const double o = __shfl_xor_sync(0xffffffffu, mx, off);
     if (__double_as_longlong(o) > __double_as_longlong(mx)) mx = o;
   }
-  if (lane == 0) atomicMax(&scale_bits, (unsigned long long)__double_as_longlong(mx));
   __syncthreads();
+  if (lane == 0) atomicMax(&scale_bits, (unsigned long long)__double_as_longlong(mx));
 
-  SPROF(0);
-  // ------------------------------------------------ dgetf2 on F (in smem)
-  for (int j = 0; j < n; ++j) {
-    if (warp == 0) {
+  // ------------------------------------------------ Gauss-Jordan sweep, one barrier per column
+  // qj (the register column of j) must be a compile-time index: unrolled outer loop over
+  // register columns, rolled inner loop over the warps that own them
+#pragma unroll
+  for (int qj = 0; qj < N / NW; ++qj)
+#pragma unroll 1
+  for (int wj = 0; wj < NW; ++wj) {
+    const int j = qj * NW + wj;
+    if (j >= n) break;
+    const int buf = j & 1;
+    if (warp == wj) {
+      // argmax |x| over rows at positions >= j; ties -> smallest position; NaN never wins
       double bv = -1.0;
       int bi = INT_MAX;
-      for (int i = j + lane; i < n; i += 32) argmax_merge(bv, bi, fabs(F[j * LDS + i]), i);
-      warp_argmax(bv, bi);
-      if (lane == 0) piv_s = (bi == INT_MAX) ? j : bi;
-    }
-    __syncthreads();
-    const int p = piv_s;
-    const double pv = F[j * LDS + p];
-    if (p != j && pv != 0.0) {
-      for (int c = tid; c < n; c += SN_THREADS) {
-        const double t = F[c * LDS + j];
-        F[c * LDS + j] = F[c * LDS + p];
-        F[c * LDS + p] = t;
+#pragma unroll
+      for (int h = 0; h < R; ++h) {
+        const int r = lane + 32 * h;
+        const double av = fabs(A[h][qj]);
+        if (r < n && pos[h] >= j && (av > bv || (av == bv && pos[h] < bi))) {
+          bv = av;
+          bi = pos[h];
+        }
       }
-      if (tid == 0) {
-        const int t = perm[j];
-        perm[j] = perm[p];
-        perm[p] = t;
+      warp_argmax_fast(bv, bi);
+      const int pp = (bi == INT_MAX) ? j : bi;   // all NaN: pivot in place
+      int oh = -1;
+#pragma unroll
+      for (int h = 0; h < R; ++h)
+        if (lane + 32 * h < n && pos[h] == pp) oh = h;
+      double mine = 0.0;
+#pragma unroll
+      for (int h = 0; h < R; ++h)
+        if (oh == h) mine = A[h][qj];
+      const unsigned m = __ballot_sync(0xffffffffu, oh >= 0);
+      const int src = __ffs(m) - 1;
+      const double pv = __shfl_sync(0xffffffffu, mine, src);
+      const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
+      const bool recip = fabs(pv) >= kSfmin;
+      const double rinv = 1.0 / pv;
+#pragma unroll
+      for (int h = 0; h < R; ++h) {
+        const int r = lane + 32 * h;
+        double l = 0.0;
+        if (r < n && r != rp && pv != 0.0) l = recip ? A[h][qj] * rinv : A[h][qj] / pv;
+        mult[buf][r] = l;
+      }
+      if (lane == 0) {
+        prow_s[buf] = rp;
+        ppos_s[buf] = pp;
+        pvs[j] = pv;
       }
     }
     __syncthreads();
-    const double piv = F[j * LDS + j];
-    if (piv != 0.0) {
-      const bool recip = fabs(piv) >= kSfmin;
-      const double rinv = 1.0 / piv;
-      for (int i = j + 1 + tid; i < n; i += SN_THREADS) {
-        const double x = F[j * LDS + i];
-        F[j * LDS + i] = recip ? x * rinv : x / piv;
+    const int rp = prow_s[buf], pp = ppos_s[buf];
+    const int srcl = rp & 31, hp = rp >> 5;
+    double lm[R];
+#pragma unroll
+    for (int h = 0; h < R; ++h) lm[h] = mult[buf][lane + 32 * h];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (warp + NW * q > j) {                // warp-uniform: columns left of j are done
+        double mine = A[0][q];
+#pragma unroll
+        for (int h = 1; h < R; ++h)
+          if (hp == h) mine = A[h][q];
+        const double u = __shfl_sync(0xffffffffu, mine, srcl);
+#pragma unroll
+        for (int h = 0; h < R; ++h) A[h][q] = fma(-lm[h], u, A[h][q]);
       }
     }
-    __syncthreads();
-    // rank-1 update, one warp per column (no index division, coalesced rows)
-    for (int c = j + 1 + warp; c < n; c += SN_THREADS / 32) {
-      const double u = F[c * LDS + j];
-      for (int i = j + 1 + lane; i < n; i += 32) F[c * LDS + i] = fma(-F[j * LDS + i], u, F[c * LDS + i]);
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      if (pos[h] == j) pos[h] = pp;           // the row at position j takes the pivot's place
+      else if (lane + 32 * h == rp) pos[h] = j;
     }
-    __syncthreads();
   }
 
-  SPROF(1);
-  // ------------------------------------------------ singularity test
+  // ------------------------------------------------ singularity test (U diagonal = the pivots)
+  __syncthreads();
   {
     const double tol = (double)n * kEps * __longlong_as_double((long long)scale_bits);
     for (int i = tid; i < n; i += SN_THREADS)
-      if (!(fabs(F[i * LDS + i]) > tol)) atomicMin(&first_bad, i);
-    __syncthreads();
-    if (tid == 0 && status != nullptr) status[blockIdx.x] = first_bad == INT_MAX ? 0 : first_bad + 1;
+      if (!(fabs(pvs[i]) > tol)) atomicMin(&first_bad, i);
   }
 
-  // ------------------------------------------------ W = P * rhs, then L, U solves
-  for (int e = tid; e < n * n; e += SN_THREADS) {
-    const int x = e % n, c = e / n;
-    const int s = perm[x];
-    W[x * LDW + c] = (mode == 1) ? (s == c ? 1.0 : 0.0) : Lb[s + (long long)c * ld];
-  }
-  __syncthreads();
-  SPROF(2);
-  // Forward (unit L) and backward (U) substitution, TPC threads per right-hand
-  // side column (one warp holds 32 / TPC columns): each step's row updates are
-  // split between them and a __syncwarp orders the steps.  Every element sees
-  // the column-serial operation sequence (fma(-x_k, L_ik, w_i) for k ascending;
-  // x_k = w_k / U_kk, then fma(-x_k, U_ik, w_i) for k descending).
-  {
-    constexpr int TPC = (SN_THREADS / NMAX) >= 8 ? 8 : (SN_THREADS / NMAX) >= 4 ? 4 : 2;
-    const int c = tid / TPC, part = tid % TPC;
-    double* w = W + c;               // element i of this column at w[i * LDW]
-    const bool col = c < n;
-    for (int k = 0; k < n; ++k) {
-      if (col) {
-        const double xk = w[k * LDW];
-        for (int i = k + 1 + part; i < n; i += TPC) w[i * LDW] = fma(-xk, F[k * LDS + i], w[i * LDW]);
-      }
-      __syncwarp();
-    }
-    for (int k = n - 1; k >= 0; --k) {
-      double xk = 0.0;
-      if (col) xk = w[k * LDW] / F[k * LDS + k];
-      __syncwarp();
-      if (col) {
-        if (part == 0) w[k * LDW] = xk;
-        for (int i = part; i < k; i += TPC) w[i * LDW] = fma(-xk, F[k * LDS + i], w[i * LDW]);
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-
-  SPROF(3);
-  if (mode == 1) {
-    for (int e = tid; e < n * n; e += SN_THREADS) {
-      const int i = e % n, c = e / n;
-      Out[i + (long long)c * ld] = W[i * LDW + c];
-    }
-    return;
-  }
-
-  // ------------------------------------------------ out = r - rt * W
-  const int tiles = (n + 3) / 4;
-  for (int tt = tid; tt < tiles * tiles; tt += SN_THREADS) {
-    const int i0 = (tt % tiles) * 4, c0 = (tt / tiles) * 4;
-    double acc[4][4];
+  // ------------------------------------------------ W(k, :) = rhs(row at position k) / u_kk
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+  for (int h = 0; h < R; ++h) {
+    const int r = lane + 32 * h;
+    if (r < n) {
+      const int k = pos[h];
+      const double piv = pvs[k];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int k = 0; k < n; ++k) {
-      double ra[4], wb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) ra[u] = (i0 + u < n) ? RT[k * LDS + i0 + u] : 0.0;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) wb[v] = (c0 + v < n) ? W[k * LDW + c0 + v] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = fma(ra[u], wb[v], acc[u][v]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int i = i0 + u, c = c0 + v;
-        if (i < n && c < n) {
-          const long long off = i + (long long)c * ld;
-          Out[off] = R[off] - acc[u][v];
+      for (int q = 0; q < Q; ++q) {
+        const int c = warp + NW * q - N;
+        if (c >= 0 && c < n) {
+          const double x = A[h][q] / piv;
+          if (mode == 1) Out[k + (long long)c * ld] = x;
+          else Ws[k * LDR + c] = x;
         }
       }
+      if (mode == 0)
+        for (int c = n; c < N; ++c) Ws[k * LDR + c] = 0.0;
+    }
   }
-  SPROF(4);
+  __syncthreads();
+  if (tid == 0 && status != nullptr) status[blockIdx.x] = first_bad == INT_MAX ? 0 : first_bad + 1;
+  if (mode == 1) return;
+
+  // ------------------------------------------------ out = r - rt * W on the tensor cores
+  cp_async_wait_all();
+  __syncthreads();
+  constexpr int MT = N / 16, NT = N / 8;
+  const int g = lane >> 2, t = lane & 3;
+  const int kmax = (n + 3) & ~3;
+  for (int tt = warp; tt < MT * NT; tt += NW) {
+    const int i0 = 16 * (tt % MT), c0 = 8 * (tt / MT);
+    if (i0 >= n || c0 >= n) continue;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < kmax; k0 += 4) {
+      const double* ra = RTs + (k0 + t) * LDR + i0 + g;
+      dmma_16x8x4(acc, ra[0], ra[8], Ws[(k0 + t) * LDR + c0 + g]);
+    }
+    const int i = i0 + g, c = c0 + 2 * t;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int ii = i + (v >> 1) * 8, cc = c + (v & 1);
+      if (ii < n && cc < n) {
+        const long long off = ii + (long long)cc * ld;
+        Out[off] = Rb[off] - acc[v];
+      }
+    }
+  }
 }
 
-template <int NMAX>
-constexpr int small_smem() { return (2 * NMAX * (NMAX + 1) + NMAX * (NMAX + 8)) * 8; }
-
-template <int NMAX>
+template <int N>
 cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int mode, int* status,
                            cudaStream_t s) {
-  const int smem = small_smem<NMAX>();
   count_launch();
-  small_node_kernel<NMAX><<<count, SN_THREADS, smem, s>>>(a, items, mode, status);
+  small_node_kernel<N><<<count, 32 * sn_warps<N>(), small_smem<N>(), s>>>(a, items, mode, status);
   return cudaGetLastError();
 }
 
 }  // namespace
-
-#ifdef BRI_SMALL_PROFILE
-void small_profile_read(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, g_small_phase, sizeof(g_small_phase));
-  unsigned long long z[8] = {0};
-  cudaMemcpyToSymbol(g_small_phase, z, sizeof(z));
-}
-#endif
 
 cudaError_t configure_small() {
   cudaError_t e = cudaFuncSetAttribute(small_node_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -45,20 +45,21 @@ BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
 
 // --------------------------------------------------------------- dinv
 // Invert the T x T diagonal blocks of the factor in slot F: unit lower (L) or
-// non-unit upper (U).  Outside [0, n) the block is the identity.  One warp per
-// column of the inverse (lane l owns rows l and l + 32), substitution by
-// shuffles: no block-wide barriers on the dependency chain.
-// dinv layout per item: [nblk][T x T column-major].
+// non-unit upper (U).  Outside [0, n) the block is the identity.  One CTA per
+// block: the block is read once into smem, each of the 8 warps owns 8 columns of
+// the inverse (lane l holds rows l and l + 32 of each) and runs their 8
+// independent substitution chains interleaved (shuffles, no block barriers on
+// the dependency chain).  Each column sees the same operation sequence as a
+// one-column-per-warp sweep.  dinv layout per item: [nblk][T x T column-major].
 constexpr int DINV_WARPS = 8;
+constexpr int DINV_COLS = T / DINV_WARPS;   // columns per warp
 
 template <bool LOWER>
 __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
                                                                int nblk, int blk0) {
   __shared__ double S[T][T + 1];   // S[c][r] = block(r, c)
-  const int cols_per_cta = DINV_WARPS;
-  const int blk = blk0 + blockIdx.x / (T / cols_per_cta), item = blockIdx.y;
-  const int c = (blockIdx.x % (T / cols_per_cta)) * cols_per_cta + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  const int blk = blk0 + blockIdx.x, item = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* F = a.base + (long long)fslots[item] * a.slot_elems;
   const int base = blk * T;
   for (int e = threadIdx.x; e < T * T; e += DINV_WARPS * 32) {
@@ -71,27 +72,44 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
     S[cc][r] = v;
   }
   __syncthreads();
-  double x0 = (lane == c) ? 1.0 : 0.0, x1 = (lane + 32 == c) ? 1.0 : 0.0;  // rows lane, lane + 32
+  double x0[DINV_COLS], x1[DINV_COLS];   // column c = warp + DINV_WARPS * q: rows lane, lane + 32
+#pragma unroll
+  for (int q = 0; q < DINV_COLS; ++q) {
+    const int c = warp + DINV_WARPS * q;
+    x0[q] = (lane == c) ? 1.0 : 0.0;
+    x1[q] = (lane + 32 == c) ? 1.0 : 0.0;
+  }
   if (LOWER) {
-#pragma unroll 4
+#pragma unroll 2
     for (int k = 0; k < T - 1; ++k) {
-      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-      if (lane > k) x0 = fma(-S[k][lane], xk, x0);
-      if (lane + 32 > k) x1 = fma(-S[k][lane + 32], xk, x1);
+      const double s0 = S[k][lane], s1 = S[k][lane + 32];
+#pragma unroll
+      for (int q = 0; q < DINV_COLS; ++q) {
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+        if (lane > k) x0[q] = fma(-s0, xk, x0[q]);
+        if (lane + 32 > k) x1[q] = fma(-s1, xk, x1[q]);
+      }
     }
   } else {
-#pragma unroll 4
+#pragma unroll 2
     for (int k = T - 1; k >= 0; --k) {
-      const double dk = S[k][k];
-      if (k >= 32) { if (lane == k - 32) x1 /= dk; } else { if (lane == k) x0 /= dk; }
-      const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
-      if (lane < k) x0 = fma(-S[k][lane], xk, x0);
-      if (lane + 32 < k) x1 = fma(-S[k][lane + 32], xk, x1);
+      const double dk = S[k][k], s0 = S[k][lane], s1 = S[k][lane + 32];
+#pragma unroll
+      for (int q = 0; q < DINV_COLS; ++q) {
+        if (k >= 32) { if (lane == k - 32) x1[q] /= dk; } else { if (lane == k) x0[q] /= dk; }
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+        if (lane < k) x0[q] = fma(-s0, xk, x0[q]);
+        if (lane + 32 < k) x1[q] = fma(-s1, xk, x1[q]);
+      }
     }
   }
-  double* out = dinv + ((long long)item * nblk + blk) * T * T + (long long)c * T;
-  out[lane] = x0;
-  out[lane + 32] = x1;
+  double* out = dinv + ((long long)item * nblk + blk) * T * T;
+#pragma unroll
+  for (int q = 0; q < DINV_COLS; ++q) {
+    const int c = warp + DINV_WARPS * q;
+    out[(long long)c * T + lane] = x0[q];
+    out[(long long)c * T + lane + 32] = x1[q];
+  }
 }
 
 // --------------------------------------------------------------- solve
@@ -406,7 +424,7 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
                         int blk0, int nblocks, cudaStream_t s) {
   const int nblk = (a.n + T - 1) / T;
   if (nblocks <= 0) nblocks = nblk - blk0;
-  dim3 grid(nblocks * (T / DINV_WARPS), count);
+  dim3 grid(nblocks, count);
   count_launch();
   if (lower)
     dinv_kernel<true><<<grid, DINV_WARPS * 32, 0, s>>>(a, fslots, dinv, nblk, blk0);

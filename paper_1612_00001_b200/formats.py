@@ -173,7 +173,12 @@ class _BlockSink:
         self._received: set = set()
         self._lock = threading.Lock()
 
+    _pinned = None
+    _pending: list = []
+
     def put(self, alpha: int, beta: int, block) -> None:
+        if self._put_device(alpha, beta, block):
+            return
         lay = self.layout
         if not (1 <= alpha <= lay.k and 1 <= beta <= lay.k):
             raise IndexOutOfRangeError(f"block ({alpha}, {beta}) outside 1..{lay.k}")
@@ -187,6 +192,44 @@ class _BlockSink:
             if r1 > r0 and c1 > c0:
                 self._canvas[r0:r1, c0:c1] = data[: r1 - r0, : c1 - c0]
             self._received.add((alpha, beta))
+
+    def _put_device(self, alpha: int, beta: int, block) -> bool:
+        """A CUDA-tensor block into a pinned canvas: one async 2-D D2H copy (bri_store_host) on
+        the block's current stream, no pageable bounce, no host-side copy; the canvas is
+        synchronized before anyone reads it.  False when this sink cannot take that path."""
+        if self._pinned is None or not getattr(block, "is_cuda", False):
+            return False
+        import ctypes
+
+        import torch
+
+        from . import _native
+
+        lay = self.layout
+        if not (1 <= alpha <= lay.k and 1 <= beta <= lay.k):
+            raise IndexOutOfRangeError(f"block ({alpha}, {beta}) outside 1..{lay.k}")
+        if tuple(block.shape) != (lay.b, lay.b) or block.dtype != torch.float64 or block.stride(1) != 1:
+            return False
+        r0, c0 = (alpha - 1) * lay.b, (beta - 1) * lay.b
+        nr, nc = min(lay.b, lay.m - r0), min(lay.b, lay.m - c0)
+        stream = torch.cuda.current_stream(block.device)
+        with self._lock:
+            if nr > 0 and nc > 0:
+                host = self._pinned.data_ptr() + 8 * (r0 * lay.m + c0)
+                _native.check(_native.load_library().bri_store_host(
+                    ctypes.c_void_p(stream.cuda_stream), ctypes.c_void_p(host), lay.m,
+                    ctypes.c_void_p(block.data_ptr()), block.stride(0), nr, nc), "bri_store_host")
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                self._pending.append((ev, block))
+            self._received.add((alpha, beta))
+        return True
+
+    def _sync(self) -> None:
+        with self._lock:
+            pending, self._pending = self._pending, []
+        for ev, _ in pending:
+            ev.synchronize()
 
     def _check_complete(self) -> None:
         k = self.layout.k
@@ -242,16 +285,50 @@ class BrimSink(_BlockSink):
 
 
 class MemorySink(_BlockSink):
-    """Collect inverse blocks into a host (m, m) array."""
+    """Collect inverse blocks into a host (m, m) array.
+
+    With a CUDA device present the canvas lives in pinned host memory (PyTorch's caching host
+    allocator, so repeated runs reuse it) and device blocks land in it by asynchronous 2-D
+    copies straight from HBM; `canvas` / `finalize()` wait for them.  Entries of blocks not
+    received read as 0, as with the reference's np.zeros canvas (formats.py:249-282)."""
 
     def __init__(self, layout):
         super().__init__(layout)
-        self._canvas = np.zeros((layout.m, layout.m))
+        m = layout.m
+        self._pending = []
+        self._pinned = None
+        try:
+            import torch
+
+            if torch.cuda.is_available() and m > 0:
+                self._pinned = torch.empty((m, m), dtype=torch.float64, pin_memory=True)
+        except Exception:  # pragma: no cover - no usable CUDA runtime: plain host canvas
+            self._pinned = None
+        self._canvas = self._pinned.numpy() if self._pinned is not None else np.zeros((m, m))
+        self._zeroed = self._pinned is None
+
+    def _zero_missing(self) -> None:
+        """Pinned canvases start uninitialized: give unreceived blocks the reference's zeros."""
+        if self._zeroed:
+            return
+        lay = self.layout
+        with self._lock:
+            got = set(self._received)
+        for a in range(1, lay.k + 1):
+            for b in range(1, lay.k + 1):
+                if (a, b) not in got:
+                    self._canvas[(a - 1) * lay.b:a * lay.b, (b - 1) * lay.b:b * lay.b] = 0.0
+        if len(got) == lay.k * lay.k:
+            self._zeroed = True
 
     @property
     def canvas(self) -> np.ndarray:
+        self._sync()
+        self._zero_missing()
         return self._canvas
 
     def finalize(self) -> np.ndarray:
+        self._sync()
         self._check_complete()
+        self._zeroed = True
         return self._canvas

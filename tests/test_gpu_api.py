@@ -466,3 +466,27 @@ def test_gaussian_provider_generated_on_device(bri):
     assert info.schedule == "bounded" and info.spills > 0
     np.testing.assert_array_equal(got[0].cpu().numpy(), bri.invert_block(bri.make_memory_provider(d8, 8), 1, 1).data)
     assert rel_err(got[0].cpu().numpy(), orc.invert_block(d8, 8, 1, 1, memo=True)) <= 1e-9
+
+
+def test_memory_sink_pinned_device_puts(bri):
+    """MemorySink with device blocks: async 2-D D2H copies into a pinned canvas (bri_store_host);
+    unreceived blocks read as zeros (reference np.zeros canvas), padding is trimmed, and the
+    result equals host-side puts of the same blocks."""
+    import torch
+
+    lay = bri.BlockLayout.for_order(10, 3)          # b = 4, l = 2: the last block is trimmed
+    sink = bri.MemorySink(lay)
+    assert sink._pinned is not None and sink._pinned.is_pinned()
+    blocks = {(a, b): torch.randn(4, 4, dtype=torch.float64, device="cuda") for a in range(1, 4) for b in range(1, 4)}
+    sink.put(1, 1, blocks[(1, 1)])
+    part = sink.canvas.copy()
+    assert np.array_equal(part[:4, :4], blocks[(1, 1)].cpu().numpy()) and not part[4:].any() and not part[:, 4:].any()
+    for (a, b), t in blocks.items():
+        sink.put(a, b, t)
+    got = sink.finalize()
+    ref = bri.MemorySink(lay)
+    for (a, b), t in blocks.items():
+        ref.put(a, b, t.cpu().numpy())
+    np.testing.assert_array_equal(got, ref.finalize())
+    with pytest.raises(bri.MissingBlocksError):
+        bri.MemorySink(lay).finalize()
