@@ -12,23 +12,23 @@
 // transpose of the reference's  r - l @ (inv(p) @ rt)  (all hats are the
 // column-major views of the row-major blocks).
 //
-// Design (latency first — a 64 x 64 node is ~0.7 MFLOP, nothing to stream):
+// Design (latency first — a 64 x 64 node is ~0.8 MFLOP, nothing to stream):
 //  * The augmented matrix [p^ | l^] (N x 2N) lives in REGISTERS: lane owns rows
 //    lane + 32h, warp w owns columns w + NW q.  No smem traffic in the sweep.
-//  * One Gauss-Jordan sweep replaces LU + forward + backward substitution (three
-//    serial sweeps): step j eliminates column j from every other row, so after
-//    N steps the solution is the right half scaled by the pivots.  The rows below
-//    the diagonal see exactly dgetf2's updates (multiplier x * (1/pivot), then
-//    fma(-l, u, a)), so the pivot sequence and the U diagonal the singularity
-//    test reads are LU's; rows above are eliminated instead of back-substituted.
+//  * The sweeps are dgetrf + dgetrs' own: step j of the factorization finds the
+//    pivot, scales the multipliers (x * (1/pivot), dgetf2) and applies the rank-1
+//    update to the trailing columns AND to the right-hand side (that is the L
+//    solve, same fma order); then a backward sweep x_k = w_k / u_kk,
+//    w_i -= u_ik x_k (k descending) solves with U.  Pivot sequence, U diagonal
+//    (the singularity test) and the solve order are LAPACK's.
 //  * Interchanges move nothing: each row keeps its physical place and carries
 //    its LAPACK *position*; the argmax breaks ties on position (idamax's first
 //    index of the permuted column), and the position bookkeeping reproduces the
 //    swap of rows j and p.
-//  * One __syncthreads per column: warp (j mod NW) owns column j, finds the pivot
-//    (REDUX argmax), writes the multipliers of all rows to a double-buffered
-//    smem vector; every warp then broadcasts the pivot row by shuffles and
-//    updates its own columns right of j.
+//  * One __syncthreads per column and sweep: warp (j mod NW) owns column j, finds
+//    the pivot (REDUX argmax), writes the multipliers of all rows to a double-
+//    buffered smem vector; every warp then broadcasts the pivot row by shuffles
+//    and updates its own columns right of j (backward: the RHS columns).
 //  * rt^ streams into smem by cp.async while the sweep runs; out = r - rt * W
 //    is DMMA (mma.sync m16n8k4 f64 -> SASS DMMA.8x8x4) from smem.
 #include <climits>
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   __syncthreads();
   if (lane == 0) atomicMax(&scale_bits, (unsigned long long)__double_as_longlong(mx));
 
-  // ------------------------------------------------ Gauss-Jordan sweep, one barrier per column
+  // ------------------------------------------------ LU + forward sweep, one barrier per column
   // qj (the register column of j) must be a compile-time index: unrolled outer loop over
   // register columns, rolled inner loop over the warps that own them
 #pragma unroll
@@ -169,11 +169,15 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
       const bool recip = fabs(pv) >= kSfmin;
       const double rinv = 1.0 / pv;
+      // dgetf2: multipliers of the rows below (positions >= j other than the pivot row)
 #pragma unroll
       for (int h = 0; h < R; ++h) {
         const int r = lane + 32 * h;
         double l = 0.0;
-        if (r < n && r != rp && pv != 0.0) l = recip ? A[h][qj] * rinv : A[h][qj] / pv;
+        if (r < n && pos[h] >= j && r != rp && pv != 0.0) {
+          l = recip ? A[h][qj] * rinv : A[h][qj] / pv;
+          A[h][qj] = l;                         // L(i, j) stays in place
+        }
         mult[buf][r] = l;
       }
       if (lane == 0) {
@@ -188,6 +192,8 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     double lm[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) lm[h] = mult[buf][lane + 32 * h];
+    // rank-1 update of the trailing matrix and the forward sweep of the right-hand side
+    // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order)
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       if (warp + NW * q > j) {                // warp-uniform: columns left of j are done
@@ -197,13 +203,59 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
           if (hp == h) mine = A[h][q];
         const double u = __shfl_sync(0xffffffffu, mine, srcl);
 #pragma unroll
-        for (int h = 0; h < R; ++h) A[h][q] = fma(-lm[h], u, A[h][q]);
+        for (int h = 0; h < R; ++h)
+          if (lm[h] != 0.0) A[h][q] = fma(-lm[h], u, A[h][q]);
       }
     }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
       if (pos[h] == j) pos[h] = pp;           // the row at position j takes the pivot's place
       else if (lane + 32 * h == rp) pos[h] = j;
+    }
+  }
+
+  // ------------------------------------------------ backward sweep (dgetrs' U solve), one barrier per column
+  //   x_k = w_k / u_kk;  w_i -= u_ik * x_k  (i < k),  k descending
+  {
+    // row -> position inverse, for the row that holds position k
+    __shared__ int row_at[N];
+#pragma unroll
+    for (int h = 0; h < R; ++h)
+      if (warp == 0 && lane + 32 * h < n) row_at[pos[h]] = lane + 32 * h;
+#pragma unroll
+    for (int qk = N / NW - 1; qk >= 0; --qk)
+#pragma unroll 1
+    for (int wk = NW - 1; wk >= 0; --wk) {
+      const int k = qk * NW + wk;
+      if (k >= n) continue;
+      const int buf = k & 1;
+      if (warp == wk) {   // U(i, k) of the rows above, from the owner of column k
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          const int r = lane + 32 * h;
+          mult[buf][r] = (r < n && pos[h] < k) ? A[h][qk] : 0.0;
+        }
+      }
+      __syncthreads();
+      const int rk = row_at[k];
+      const int srcl = rk & 31, hk = rk >> 5;
+      const double ukk = pvs[k];
+      double um[R];
+#pragma unroll
+      for (int h = 0; h < R; ++h) um[h] = mult[buf][lane + 32 * h];
+#pragma unroll
+      for (int q = Q / 2; q < Q; ++q) {       // right-hand-side columns only
+        double mine = A[0][q];
+#pragma unroll
+        for (int h = 1; h < R; ++h)
+          if (hk == h) mine = A[h][q];
+        const double x = __shfl_sync(0xffffffffu, mine, srcl) / ukk;
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          if (lane + 32 * h == rk) A[h][q] = x;
+          else if (um[h] != 0.0) A[h][q] = fma(-um[h], x, A[h][q]);
+        }
+      }
     }
   }
 
@@ -215,18 +267,17 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       if (!(fabs(pvs[i]) > tol)) atomicMin(&first_bad, i);
   }
 
-  // ------------------------------------------------ W(k, :) = rhs(row at position k) / u_kk
+  // ------------------------------------------------ W(k, :) = the solved row at position k
 #pragma unroll
   for (int h = 0; h < R; ++h) {
     const int r = lane + 32 * h;
     if (r < n) {
       const int k = pos[h];
-      const double piv = pvs[k];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const int c = warp + NW * q - N;
         if (c >= 0 && c < n) {
-          const double x = A[h][q] / piv;
+          const double x = A[h][q];
           if (mode == 1) Out[k + (long long)c * ld] = x;
           else Ws[k * LDR + c] = x;
         }
