@@ -74,6 +74,9 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int count;      // batch size (set by launch_gemm)
   int max_ctas;   // > 0: persistent launch with at most this many CTAs
+  int overlap;    // 1: persistent launch, one CTA per SM, whose epilogue (straight from the
+                  // accumulators) overlaps the next tile's TMA loads; only where nothing runs
+                  // concurrently on other streams (it holds every SM until the batch is done)
 };
 
 int gemm_smem_bytes();

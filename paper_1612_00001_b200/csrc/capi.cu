@@ -208,9 +208,10 @@ LuScratch lu_scratch(void* base, const LuLayout& L) {
 
 int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, int M, int N, int K,
               int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta,
-              int max_ctas = 0) {
+              int max_ctas = 0, int overlap = 0) {
   GemmParams p{};
   p.max_ctas = max_ctas;
+  p.overlap = overlap;
   p.base = ar->v.base;
   p.ld = ar->v.ld;
   p.slot_elems = ar->v.slot_elems;
@@ -533,7 +534,7 @@ int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, d
 // columns >= r0 + nr are skipped entirely and the leaves start at each
 // column's diagonal.
 int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, int count, bool lower,
-             int r0, int nr, int nrhs, const double* dinv, bool tri = false) {
+             int r0, int nr, int nrhs, const double* dinv, bool tri = false, int overlap = 0) {
   const int ncol = tri ? (r0 + nr < nrhs ? r0 + nr : nrhs) : nrhs;
   if (nr <= TRSM_LEAF) {
     BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, ar->v, fw, count, dinv, lower, r0, nr, 0, ncol, tri, s));
@@ -542,28 +543,30 @@ int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, i
   int h = ((nr / 2) + TRSM_BLOCK - 1) / TRSM_BLOCK * TRSM_BLOCK;
   if (h >= nr) h = nr - TRSM_BLOCK;
   if (lower) {
-    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs, dinv, tri)) return rc;
+    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs, dinv, tri, overlap)) return rc;
     // W[r0+h : r0+nr, :] -= L[r0+h : r0+nr, r0 : r0+h] * W[r0 : r0+h, :]
     const int gcol = tri ? (r0 + h < nrhs ? r0 + h : nrhs) : nrhs;
-    if (int rc = gemm_call(ar, s, gemm_fw, count, nr - h, gcol, h, r0 + h, r0, r0, 0, r0 + h, 0, -1.0, 1.0))
+    if (int rc = gemm_call(ar, s, gemm_fw, count, nr - h, gcol, h, r0 + h, r0, r0, 0, r0 + h, 0, -1.0, 1.0, 0,
+                           overlap))
       return rc;
-    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs, dinv, tri);
+    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs, dinv, tri, overlap);
   }
-  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs, dinv)) return rc;
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs, dinv, false, overlap)) return rc;
   // W[r0 : r0+h, :] -= U[r0 : r0+h, r0+h : r0+nr] * W[r0+h : r0+nr, :]
-  if (int rc = gemm_call(ar, s, gemm_fw, count, h, nrhs, nr - h, r0, r0 + h, r0 + h, 0, r0, 0, -1.0, 1.0))
+  if (int rc = gemm_call(ar, s, gemm_fw, count, h, nrhs, nr - h, r0, r0 + h, r0 + h, 0, r0, 0, -1.0, 1.0, 0,
+                         overlap))
     return rc;
-  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs, dinv);
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs, dinv, false, overlap);
 }
 
 // Both sweeps of dgetrs on W (already row-permuted): L then U.
 int getrs_sweeps(bri_arena* ar, cudaStream_t s, const int* dev_f, const int* fw, const int* gemm_fw, int count,
-                 bool tri_rhs = false, bool after_getrf = false) {
+                 bool tri_rhs = false, bool after_getrf = false, int overlap = 0) {
   double *dl = nullptr, *du = nullptr;
   if (int rc = make_dinv(ar, s, dev_f, count, &dl, &du, after_getrf)) return rc;
   const int n = ar->v.n;
-  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, 0, n, n, dl, tri_rhs)) return rc;
-  return trsm_rec(ar, s, fw, gemm_fw, count, false, 0, n, n, du);
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, 0, n, n, dl, tri_rhs, overlap)) return rc;
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, 0, n, n, du, false, overlap);
 }
 
 // Run a hot-path kernel sequence as a CUDA graph.  The sequence for a given
@@ -856,7 +859,7 @@ int bri_gemm(bri_arena* ar, void* stream, int count, const int* items, int M, in
   std::vector<int> h(items, items + 4 * count);
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
-  return gemm_call(ar, s, dev, count, M, N, K, a_r0, a_c0, b_r0, b_c0, c_r0, c_c0, alpha, beta);
+  return gemm_call(ar, s, dev, count, M, N, K, a_r0, a_c0, b_r0, b_c0, c_r0, c_c0, alpha, beta, 0, 1);
 }
 
 int bri_axpby(bri_arena* ar, void* stream, int count, const int* items, double alpha, double beta) {
@@ -1224,11 +1227,11 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
     if (ns > 0) {   // W = U^-1 L^-1 P l with the permutation of the solve's factor
       if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
       BRI_CHECK(launch_permcopy(ar->v, d_lw, ns, sc.pi, n, false, st, d_fidx));
-      if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false)) return rc;
+      if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false, 1)) return rc;
     }
     if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
     if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
-    if (ng > 0) return gemm_call(ar, st, d_g, ng, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0);
+    if (ng > 0) return gemm_call(ar, st, d_g, ng, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0, 0, 1);
     return 0;
   };
   std::vector<uintptr_t> key = graph_key(2, ar, ng, dev);

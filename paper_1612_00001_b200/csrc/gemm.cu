@@ -197,25 +197,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   // caps the CTA count, e.g. to leave SMs to a concurrent critical path); the
   // ring position g0 and its mbarrier phases run on across a CTA's tiles.
   int g0 = 0;
+  auto issue_tile = [&](int tile, int kt, int gbase) {
+    const int item = tile / tiles_per_item, rem = tile % tiles_per_item;
+    const int* it = p.items + 4 * item;
+    const int m0 = (rem % p.tiles_m) * BM, n0 = (rem / p.tiles_m) * BN;
+    const int s = (gbase + kt) % STAGES;
+    tile_issue<BM, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, it[0],
+                       p.b_r0 + kt * BK, p.b_c0 + n0, it[1]);
+  };
+  // the first STAGES k-tiles of a tile, each once its ring slot is released
+  auto issue_head = [&](int tile, int gbase) {
+    for (int kt = 0; kt < STAGES && kt < KT; ++kt) {
+      const int gg = gbase + kt;
+      if (gg >= STAGES) mbar_wait(&empty[gg % STAGES], ((gg / STAGES) - 1) & 1);
+      issue_tile(tile, kt, gbase);
+    }
+  };
+  if (producer && blockIdx.x < total) issue_head(blockIdx.x, 0);
   for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
     const int item = tile / tiles_per_item, rem = tile % tiles_per_item;
     const int* it = p.items + 4 * item;
-    const int sa = it[0], sb = it[1], sc_in = it[2], sc_out = it[3];
+    const int sc_in = it[2], sc_out = it[3];
     const int tm = rem % p.tiles_m;
     const int tn = rem / p.tiles_m;
     const int m0 = tm * BM, n0 = tn * BN;
-    auto issue = [&](int kt) {
-      const int s = (g0 + kt) % STAGES;
-      tile_issue<BM, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, sa,
-                         p.b_r0 + kt * BK, p.b_c0 + n0, sb);
-    };
-    if (producer) {
-      for (int kt = 0; kt < STAGES && kt < KT; ++kt) {
-        const int gg = g0 + kt;
-        if (gg >= STAGES) mbar_wait(&empty[gg % STAGES], ((gg / STAGES) - 1) & 1);
-        issue(kt);
-      }
-    }
     WarpAcc<WTM / 16, WTN / 8> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
@@ -223,9 +228,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&full[s], (gg / STAGES) & 1);
       const uint8_t* sA = smem + s * STAGE_BYTES;
       if (p.K - kt * BK >= BK)
-      acc.template mma_stage<true>(sA, sA + StageGeom<BM, BN>::A_BYTES, BK, wm0, wn0, lane);
-    else
-      acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
+        acc.template mma_stage<true>(sA, sA + StageGeom<BM, BN>::A_BYTES, BK, wm0, wn0, lane);
+      else
+        acc.mma_stage(sA, sA + StageGeom<BM, BN>::A_BYTES, p.K - kt * BK, wm0, wn0, lane);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (producer && kt >= 1) {
@@ -233,11 +238,52 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (kp + STAGES < KT) {
           const int gp = g0 + kp;
           mbar_wait(&empty[gp % STAGES], (gp / STAGES) & 1);
-          issue(kp + STAGES);
+          issue_tile(tile, kp + STAGES, g0);
         }
       }
     }
     g0 += KT;
+    double* cout = p.base + (long long)sc_out * p.slot_elems;
+    const double* cin = p.base + (long long)sc_in * p.slot_elems;
+    const bool read_c = p.beta != 0.0;
+    if (p.overlap) {
+      // the next tile's first k-tiles load while this tile's epilogue runs
+      if (producer && tile + (int)gridDim.x < total) issue_head(tile + gridDim.x, g0);
+      // epilogue straight from the accumulators: per store instruction a warp writes
+      // 4 columns x 8 contiguous rows (whole 32-byte sectors); same arithmetic as the
+      // staged path, fma(beta, C_in, alpha * acc).  C_in may alias C_out: every element
+      // is read and written by the same thread.
+      const int g = lane >> 2, t = lane & 3;
+      constexpr int JC = 2;   // fragment columns per round trip (register budget: 128 per thread)
+#pragma unroll
+      for (int i = 0; i < WTM / 16; ++i)
+#pragma unroll
+      for (int j0 = 0; j0 < WTN / 8; j0 += JC) {
+        double old[JC][4];
+#pragma unroll
+        for (int j = 0; j < JC; ++j)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int grow = m0 + wm0 + 16 * i + g + ((v >> 1) << 3);
+            const int gcol = n0 + wn0 + 8 * (j0 + j) + 2 * t + (v & 1);
+            const bool ok = grow < p.M && gcol < p.N;
+            old[j][v] = (ok && read_c) ? cin[(long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld] : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < JC; ++j)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int grow = m0 + wm0 + 16 * i + g + ((v >> 1) << 3);
+            const int gcol = n0 + wn0 + 8 * (j0 + j) + 2 * t + (v & 1);
+            if (grow < p.M && gcol < p.N) {
+              const double val = p.alpha * acc.c[i][j0 + j][v];
+              cout[(long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld] =
+                  read_c ? fma(p.beta, old[j][v], val) : val;
+            }
+          }
+      }
+      continue;
+    }
 
     // ---------------------------------------------------------- epilogue
     // Stage alpha*acc through smem, then stream whole columns (contiguous in
@@ -247,9 +293,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     double* tile_s = reinterpret_cast<double*>(smem);
     acc.to_smem(tile_s, LDT, wm0, wn0, lane, p.alpha);
     __syncthreads();
-    double* cout = p.base + (long long)sc_out * p.slot_elems;
-    const double* cin = p.base + (long long)sc_in * p.slot_elems;
-    const bool read_c = p.beta != 0.0;
     for (int c = warp; c < BN; c += 2 * NUM_WARPS) {
       double v[2][4], old[2][4];
       long long off[2][4];
@@ -277,6 +320,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // the next tile's TMA writes (async proxy) reuse this smem
     fence_proxy_async_smem();
     __syncthreads();
+    if (producer && tile + (int)gridDim.x < total) issue_head(tile + gridDim.x, g0);
   }
 }
 
@@ -421,6 +465,19 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   }
   p.count = count;
   long long ctas = (long long)p.tiles_m * p.tiles_n * count;
+  static const int overlap_env = env_int("BRI_GEMM_OVERLAP", 1);
+  static const int num_sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  // overlapped persistent launch: more than one wave, nothing concurrent (caller's flag)
+  p.overlap = (p.overlap && overlap_env && p.max_ctas <= 0 && ctas > num_sms) ? 1 : 0;
+  if (p.overlap) {
+    count_launch();
+    gemm_persistent_kernel<<<dim3((unsigned)num_sms), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+    return cudaGetLastError();
+  }
   if (p.max_ctas > 0 && ctas > p.max_ctas) ctas = p.max_ctas;
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   count_launch();
