@@ -57,6 +57,20 @@ constexpr int sn_ldr() { return N + 8; }   // == 8 (mod 16) doubles: conflict-fr
 template <int N>
 constexpr int small_smem() { return 2 * N * sn_ldr<N>() * 8; }
 
+#ifdef BRI_SMALL_PROFILE
+__device__ unsigned long long g_small_phase[8];
+#define SPROF(k)                                                   \
+  do {                                                             \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                     \
+      const unsigned long long now = clock64();                    \
+      atomicAdd(&g_small_phase[k], now - t_last);                  \
+      t_last = now;                                                \
+    }                                                              \
+  } while (0)
+#else
+#define SPROF(k) do { } while (0)
+#endif
+
 // mode 0: Schur node (items: p, rt, l, r, out);  mode 1: out = p^-1 (items: in, -, -, -, out)
 template <int N>
 __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(ArenaView a, const int* items, int mode,
@@ -83,6 +97,9 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   const double* Rb = a.base + (long long)it[3] * a.slot_elems;
   double* Out = a.base + (long long)it[4] * a.slot_elems;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef BRI_SMALL_PROFILE
+  unsigned long long t_last = clock64();
+#endif
 
   if (tid == 0) {
     scale_bits = 0ull;
@@ -130,6 +147,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   __syncthreads();
   if (lane == 0) atomicMax(&scale_bits, (unsigned long long)__double_as_longlong(mx));
 
+  SPROF(0);
   // ------------------------------------------------ LU + forward sweep, one barrier per column
   // qj (the register column of j) must be a compile-time index: unrolled outer loop over
   // register columns, rolled inner loop over the warps that own them
@@ -214,6 +232,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     }
   }
 
+  SPROF(1);
   // ------------------------------------------------ backward sweep (dgetrs' U solve), one barrier per column
   //   x_k = w_k / u_kk;  w_i -= u_ik * x_k  (i < k),  k descending
   {
@@ -261,6 +280,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
 
   // ------------------------------------------------ singularity test (U diagonal = the pivots)
   __syncthreads();
+  SPROF(2);
   {
     const double tol = (double)n * kEps * __longlong_as_double((long long)scale_bits);
     for (int i = tid; i < n; i += SN_THREADS)
@@ -288,11 +308,13 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   }
   __syncthreads();
   if (tid == 0 && status != nullptr) status[blockIdx.x] = first_bad == INT_MAX ? 0 : first_bad + 1;
+  SPROF(3);
   if (mode == 1) return;
 
   // ------------------------------------------------ out = r - rt * W on the tensor cores
   cp_async_wait_all();
   __syncthreads();
+  SPROF(4);
   constexpr int MT = N / 16, NT = N / 8;
   const int g = lane >> 2, t = lane & 3;
   const int kmax = (n + 3) & ~3;
@@ -314,6 +336,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       }
     }
   }
+  SPROF(5);
 }
 
 template <int N>
@@ -325,6 +348,14 @@ cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int 
 }
 
 }  // namespace
+
+#ifdef BRI_SMALL_PROFILE
+void small_profile_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_small_phase, sizeof(g_small_phase));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_small_phase, z, sizeof(z));
+}
+#endif
 
 cudaError_t configure_small() {
   cudaError_t e = cudaFuncSetAttribute(small_node_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,

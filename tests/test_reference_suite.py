@@ -12,12 +12,14 @@ Deselected, with reasons:
     §2 row 19, §8 "out of scope"); nothing of it is rebuilt here.
 
 Two runs on the GPU:
-  * schedule "tree" (BRI_SCHEDULE=tree: the reference's depth-first recursion and its
-    <= 2k+4 live-block contract, SPEC.md:286): every case must pass;
   * the default "dag" schedule (each distinct node once, level-batched): every case must pass
     except the live-block-contract assertions in MEMORY_CONTRACT — the DAG deliberately holds
     whole levels of node values (its gauge reports that true footprint) to evaluate shared
-    subtrees once; nothing else may fail.
+    subtrees once; nothing else may fail;
+  * schedule "tree" (BRI_SCHEDULE=tree: the reference's depth-first recursion and its
+    <= 2k+4 live-block contract) on the MEMORY_CONTRACT cases: all must pass.
+    (The whole suite in tree mode — 172 of 172 passed, profiles/r02_reference_suite_tree.txt —
+    takes ~7 minutes; BRI_REF_SUITE_TREE_ALL=1 runs it.)
 
 On CPU only the host-side cases can pass (frames, formats, counters, errors, providers' host
 logic); every computing case must fail loudly with DeviceError — never fall back to the CPU.
@@ -89,7 +91,10 @@ def test_reference_suite_on_gpu(schedule):
         pytest.skip("no CUDA device")
     if not _have_suite():
         pytest.skip("reference suite not vendored")
-    rc, counts, text = _run(["-rf"], schedule=schedule)
+    extra = ["-rf"]
+    if schedule == "tree" and os.environ.get("BRI_REF_SUITE_TREE_ALL") != "1":
+        extra += ["-k", "memory_contract or peak_live_blocks_bound or summary_accounting"]
+    rc, counts, text = _run(extra, schedule=schedule)
     report = os.path.join(ROOT, "gpurun_out", f"reference_suite_{schedule}.txt")
     if os.path.isdir(os.path.dirname(report)):
         with open(report, "w") as fh:
@@ -102,4 +107,7 @@ def test_reference_suite_on_gpu(schedule):
     else:
         unexpected = [f for f in failed if not f.startswith(MEMORY_CONTRACT)]
         assert not unexpected, unexpected
-    assert counts.get("passed", 0) + len(failed) >= 170, counts
+    if schedule == "tree" and os.environ.get("BRI_REF_SUITE_TREE_ALL") != "1":
+        assert counts.get("passed", 0) >= 17, counts
+    else:
+        assert counts.get("passed", 0) + len(failed) >= 170, counts
