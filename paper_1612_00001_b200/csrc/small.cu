@@ -18,8 +18,9 @@
 //  * The sweeps are dgetrf + dgetrs' own: step j of the factorization finds the
 //    pivot, scales the multipliers (x * (1/pivot), dgetf2) and applies the rank-1
 //    update to the trailing columns AND to the right-hand side (that is the L
-//    solve, same fma order); then a backward sweep x_k = w_k / u_kk,
-//    w_i -= u_ik x_k (k descending) solves with U.  Pivot sequence, U diagonal
+//    solve, same fma order); then a backward sweep x_k = w_k * (1/u_kk) (OpenBLAS'
+//    trsm kernels multiply by the inverted diagonal), w_i -= u_ik x_k (k
+//    descending) solves with U.  Pivot sequence, U diagonal
 //    (the singularity test) and the solve order are LAPACK's.
 //  * Interchanges move nothing: each row keeps its physical place and carries
 //    its LAPACK *position*; the argmax breaks ties on position (idamax's first
@@ -212,17 +213,19 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     for (int h = 0; h < R; ++h) lm[h] = mult[buf][lane + 32 * h];
     // rank-1 update of the trailing matrix and the forward sweep of the right-hand side
     // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order)
+    // branch-free (a shuffle under a per-column branch serialises the columns behind
+    // convergence barriers): every column shuffles, only live columns (right of j) update
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      if (warp + NW * q > j) {                // warp-uniform: columns left of j are done
-        double mine = A[0][q];
+      const bool live = warp + NW * q > j;    // warp-uniform: columns left of j are done
+      double mine = A[0][q];
 #pragma unroll
-        for (int h = 1; h < R; ++h)
-          if (hp == h) mine = A[h][q];
-        const double u = __shfl_sync(0xffffffffu, mine, srcl);
+      for (int h = 1; h < R; ++h) mine = (hp == h) ? A[h][q] : mine;
+      const double u = __shfl_sync(0xffffffffu, mine, srcl);
 #pragma unroll
-        for (int h = 0; h < R; ++h)
-          if (lm[h] != 0.0) A[h][q] = fma(-lm[h], u, A[h][q]);
+      for (int h = 0; h < R; ++h) {
+        const double upd = fma(-lm[h], u, A[h][q]);
+        A[h][q] = (live && lm[h] != 0.0) ? upd : A[h][q];
       }
     }
 #pragma unroll
@@ -258,7 +261,9 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       __syncthreads();
       const int rk = row_at[k];
       const int srcl = rk & 31, hk = rk >> 5;
-      const double ukk = pvs[k];
+      // x_k = w_k * (1 / u_kk): one division per column of U, as OpenBLAS' trsm
+      // kernels do with their inverted diagonal
+      const double rkk = 1.0 / pvs[k];
       double um[R];
 #pragma unroll
       for (int h = 0; h < R; ++h) um[h] = mult[buf][lane + 32 * h];
@@ -266,13 +271,12 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       for (int q = Q / 2; q < Q; ++q) {       // right-hand-side columns only
         double mine = A[0][q];
 #pragma unroll
-        for (int h = 1; h < R; ++h)
-          if (hk == h) mine = A[h][q];
-        const double x = __shfl_sync(0xffffffffu, mine, srcl) / ukk;
+        for (int h = 1; h < R; ++h) mine = (hk == h) ? A[h][q] : mine;
+        const double x = __shfl_sync(0xffffffffu, mine, srcl) * rkk;
 #pragma unroll
         for (int h = 0; h < R; ++h) {
-          if (lane + 32 * h == rk) A[h][q] = x;
-          else if (um[h] != 0.0) A[h][q] = fma(-um[h], x, A[h][q]);
+          const double upd = fma(-um[h], x, A[h][q]);
+          A[h][q] = (lane + 32 * h == rk) ? x : (um[h] != 0.0 ? upd : A[h][q]);
         }
       }
     }
