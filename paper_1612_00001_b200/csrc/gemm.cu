@@ -465,7 +465,10 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   }
   p.count = count;
   long long ctas = (long long)p.tiles_m * p.tiles_n * count;
-  static const int overlap_env = env_int("BRI_GEMM_OVERLAP", 1);
+  // opt-in (BRI_GEMM_OVERLAP=1): measured slower — level batch of 148 b=1024 nodes 9.77 vs
+  // 9.56 ms, config 3 1031 vs 1016 ms: the register epilogue's 64-byte column pieces cost
+  // more than the ~4% of a K=1024 tile the overlap could hide
+  static const int overlap_env = env_int("BRI_GEMM_OVERLAP", 0);
   static const int num_sms = [] {
     int dev = 0, n = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);

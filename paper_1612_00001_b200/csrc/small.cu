@@ -150,8 +150,69 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
 
   SPROF(0);
   // ------------------------------------------------ LU + forward sweep, one barrier per column
+  // Pivot step for column jn held in register column qn by the calling warp: argmax
+  // |x| over rows at positions >= jn (ties -> smallest position, NaN never wins), the
+  // signed pivot, dgetf2's multipliers x * (1/pivot) of the rows below (kept in place
+  // as L(i, jn) and published to smem for every warp), the pivot row and position.
+  auto pivot_step = [&](int jn, int qn) {
+    const int bufn = jn & 1;
+    double bv = -1.0;
+    int bi = INT_MAX;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int r = lane + 32 * h;
+      const double av = fabs(A[h][qn]);
+      if (r < n && pos[h] >= jn && (av > bv || (av == bv && pos[h] < bi))) {
+        bv = av;
+        bi = pos[h];
+      }
+    }
+    warp_argmax_fast(bv, bi);
+    const int pp = (bi == INT_MAX) ? jn : bi;   // all NaN: pivot in place
+    int oh = -1;
+#pragma unroll
+    for (int h = 0; h < R; ++h)
+      if (lane + 32 * h < n && pos[h] == pp) oh = h;
+    double mine = 0.0;
+#pragma unroll
+    for (int h = 0; h < R; ++h)
+      if (oh == h) mine = A[h][qn];
+    const unsigned m = __ballot_sync(0xffffffffu, oh >= 0);
+    const int src = __ffs(m) - 1;
+    const double pv = __shfl_sync(0xffffffffu, mine, src);
+    const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
+    const bool recip = fabs(pv) >= kSfmin;
+    const double rinv = 1.0 / pv;
+#pragma unroll
+    for (int h = 0; h < R; ++h) {
+      const int r = lane + 32 * h;
+      double l = 0.0;
+      if (r < n && pos[h] >= jn && r != rp && pv != 0.0) {
+        l = recip ? A[h][qn] * rinv : A[h][qn] / pv;
+        A[h][qn] = l;
+      }
+      mult[bufn][r] = l;
+    }
+    if (lane == 0) {
+      prow_s[bufn] = rp;
+      ppos_s[bufn] = pp;
+      pvs[jn] = pv;
+    }
+  };
+  // column q of this warp for step j: a_iq -= l_i * u_jq (u_jq from the pivot row's lane)
+  auto update_col = [&](int q, const double (&lm)[R], int srcl, int hp) {
+    double mine = A[0][q];
+#pragma unroll
+    for (int h = 1; h < R; ++h) mine = (hp == h) ? A[h][q] : mine;
+    const double u = __shfl_sync(0xffffffffu, mine, srcl);
+#pragma unroll
+    for (int h = 0; h < R; ++h) A[h][q] = fma(-lm[h], u, A[h][q]);   // l = 0: unchanged
+  };
+  if (warp == 0 && n > 0) pivot_step(0, 0);
   // qj (the register column of j) must be a compile-time index: unrolled outer loop over
-  // register columns, rolled inner loop over the warps that own them
+  // register columns, rolled inner loop over the warps that own them.  Lookahead: the
+  // owner of column j+1 updates that column first and publishes step j+1's pivot before
+  // its other columns, so the pivot search leaves the critical path of the update.
 #pragma unroll
   for (int qj = 0; qj < N / NW; ++qj)
 #pragma unroll 1
@@ -159,114 +220,71 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     const int j = qj * NW + wj;
     if (j >= n) break;
     const int buf = j & 1;
-    if (warp == wj) {
-      // argmax |x| over rows at positions >= j; ties -> smallest position; NaN never wins
-      double bv = -1.0;
-      int bi = INT_MAX;
-#pragma unroll
-      for (int h = 0; h < R; ++h) {
-        const int r = lane + 32 * h;
-        const double av = fabs(A[h][qj]);
-        if (r < n && pos[h] >= j && (av > bv || (av == bv && pos[h] < bi))) {
-          bv = av;
-          bi = pos[h];
-        }
-      }
-      warp_argmax_fast(bv, bi);
-      const int pp = (bi == INT_MAX) ? j : bi;   // all NaN: pivot in place
-      int oh = -1;
-#pragma unroll
-      for (int h = 0; h < R; ++h)
-        if (lane + 32 * h < n && pos[h] == pp) oh = h;
-      double mine = 0.0;
-#pragma unroll
-      for (int h = 0; h < R; ++h)
-        if (oh == h) mine = A[h][qj];
-      const unsigned m = __ballot_sync(0xffffffffu, oh >= 0);
-      const int src = __ffs(m) - 1;
-      const double pv = __shfl_sync(0xffffffffu, mine, src);
-      const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
-      const bool recip = fabs(pv) >= kSfmin;
-      const double rinv = 1.0 / pv;
-      // dgetf2: multipliers of the rows below (positions >= j other than the pivot row)
-#pragma unroll
-      for (int h = 0; h < R; ++h) {
-        const int r = lane + 32 * h;
-        double l = 0.0;
-        if (r < n && pos[h] >= j && r != rp && pv != 0.0) {
-          l = recip ? A[h][qj] * rinv : A[h][qj] / pv;
-          A[h][qj] = l;                         // L(i, j) stays in place
-        }
-        mult[buf][r] = l;
-      }
-      if (lane == 0) {
-        prow_s[buf] = rp;
-        ppos_s[buf] = pp;
-        pvs[j] = pv;
-      }
-    }
     __syncthreads();
     const int rp = prow_s[buf], pp = ppos_s[buf];
     const int srcl = rp & 31, hp = rp >> 5;
     double lm[R];
 #pragma unroll
     for (int h = 0; h < R; ++h) lm[h] = mult[buf][lane + 32 * h];
-    // rank-1 update of the trailing matrix and the forward sweep of the right-hand side
-    // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order)
-    // branch-free (a shuffle under a per-column branch serialises the columns behind
-    // convergence barriers): every column shuffles, only live columns (right of j) update
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const bool live = warp + NW * q > j;    // warp-uniform: columns left of j are done
-      double mine = A[0][q];
-#pragma unroll
-      for (int h = 1; h < R; ++h) mine = (hp == h) ? A[h][q] : mine;
-      const double u = __shfl_sync(0xffffffffu, mine, srcl);
-#pragma unroll
-      for (int h = 0; h < R; ++h) {
-        const double upd = fma(-lm[h], u, A[h][q]);
-        A[h][q] = (live && lm[h] != 0.0) ? upd : A[h][q];
-      }
-    }
 #pragma unroll
     for (int h = 0; h < R; ++h) {
       if (pos[h] == j) pos[h] = pp;           // the row at position j takes the pivot's place
       else if (lane + 32 * h == rp) pos[h] = j;
     }
+    const bool wrap = (wj == NW - 1);         // column j+1 sits in the next register column
+    const bool la = (j + 1 < n) && warp == (wrap ? 0 : wj + 1);
+    if (la) {
+      if (!wrap) {
+        update_col(qj, lm, srcl, hp);
+        pivot_step(j + 1, qj);
+      } else if (qj + 1 < N / NW) {
+        update_col(qj + 1, lm, srcl, hp);
+        pivot_step(j + 1, qj + 1);
+      }
+    }
+    // rank-1 update of the trailing matrix and the forward sweep of the right-hand side
+    // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order); register
+    // columns left of qj are dead for every warp (compile-time), column qj is live only right
+    // of j, and the lookahead column is already done
+#pragma unroll
+    for (int q = qj; q < Q; ++q) {
+      const int c = warp + NW * q;
+      const bool done = (la && c == j + 1);
+      if (q == qj || q == qj + 1) {
+        if (c > j && !done) update_col(q, lm, srcl, hp);
+      } else {
+        update_col(q, lm, srcl, hp);
+      }
+    }
   }
 
   SPROF(1);
-  // ------------------------------------------------ backward sweep (dgetrs' U solve), one barrier per column
-  //   x_k = w_k / u_kk;  w_i -= u_ik * x_k  (i < k),  k descending
+  // ------------------------------------------------ backward sweep (dgetrs' U solve), no barriers
+  //   x_k = w_k * (1/u_kk);  w_i -= u_ik x_k  (i < k),  k descending.  U is static by now:
+  //   its columns go to smem once (the owner of column k writes U(., k) by physical row),
+  //   and every warp then solves its own right-hand-side columns independently.
   {
-    // row -> position inverse, for the row that holds position k
     __shared__ int row_at[N];
+    double* Us = Ws;   // U(r, k) at Us[k * LDR + r] (physical row r); Ws is rebuilt afterwards
+    __syncthreads();
 #pragma unroll
-    for (int h = 0; h < R; ++h)
-      if (warp == 0 && lane + 32 * h < n) row_at[pos[h]] = lane + 32 * h;
+    for (int h = 0; h < R; ++h) {
+      const int r = lane + 32 * h;
+      if (warp == 0 && r < n) row_at[pos[h]] = r;
 #pragma unroll
-    for (int qk = N / NW - 1; qk >= 0; --qk)
-#pragma unroll 1
-    for (int wk = NW - 1; wk >= 0; --wk) {
-      const int k = qk * NW + wk;
-      if (k >= n) continue;
-      const int buf = k & 1;
-      if (warp == wk) {   // U(i, k) of the rows above, from the owner of column k
-#pragma unroll
-        for (int h = 0; h < R; ++h) {
-          const int r = lane + 32 * h;
-          mult[buf][r] = (r < n && pos[h] < k) ? A[h][qk] : 0.0;
-        }
+      for (int q = 0; q < Q / 2; ++q) {      // matrix columns of this warp
+        const int c = warp + NW * q;
+        if (c < n && r < N) Us[c * LDR + r] = (r < n && pos[h] < c) ? A[h][q] : 0.0;
       }
-      __syncthreads();
+    }
+    __syncthreads();
+    for (int k = n - 1; k >= 0; --k) {
       const int rk = row_at[k];
       const int srcl = rk & 31, hk = rk >> 5;
-      // x_k = w_k * (1 / u_kk): one division per column of U, as OpenBLAS' trsm
-      // kernels do with their inverted diagonal
       const double rkk = 1.0 / pvs[k];
       double um[R];
 #pragma unroll
-      for (int h = 0; h < R; ++h) um[h] = mult[buf][lane + 32 * h];
+      for (int h = 0; h < R; ++h) um[h] = Us[k * LDR + lane + 32 * h];
 #pragma unroll
       for (int q = Q / 2; q < Q; ++q) {       // right-hand-side columns only
         double mine = A[0][q];
@@ -274,10 +292,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
         for (int h = 1; h < R; ++h) mine = (hk == h) ? A[h][q] : mine;
         const double x = __shfl_sync(0xffffffffu, mine, srcl) * rkk;
 #pragma unroll
-        for (int h = 0; h < R; ++h) {
-          const double upd = fma(-um[h], x, A[h][q]);
-          A[h][q] = (lane + 32 * h == rk) ? x : (um[h] != 0.0 ? upd : A[h][q]);
-        }
+        for (int h = 0; h < R; ++h) A[h][q] = (lane + 32 * h == rk) ? x : fma(-um[h], x, A[h][q]);
       }
     }
   }
