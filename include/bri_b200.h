@@ -93,6 +93,19 @@ int bri_level_batch_gated(bri_arena* arena, void* stream, int nf, const int* fit
                           int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr);
 
 /*
+ * The general level batch: as bri_level_batch_gated, plus right-side solves for
+ * pivots whose nodes share fewer distinct rt than l operands (the reference's own
+ * association (rt · inv(p)) · l, engine.py:167-174, in X-world): C = rt^ p^-1 solved once
+ * per distinct (pivot, rt), then out = r - C * l.  titems: 2 ints (factor index into
+ * fitems, Ft scratch slot) per factor used on that side; ritems: 4 ints (index into
+ * titems, rt slot, S scratch slot, C output slot); GEMM items of those nodes are
+ * (C, l, r, out).  nt = nr = 0 is bri_level_batch_gated.
+ */
+int bri_level_batch_ex(bri_arena* arena, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                       int nt, const int* titems, int nr, const int* ritems, int ng, const int* gitems, int* fstatus,
+                       void* ev_l, void* ev_rtr);
+
+/*
  * Block inverses, batched — replaces core.py:238-263 (invert_dense).
  * items: 3 ints per block: slots (in, f, out); f is scratch; in is not modified.
  * status (device, count ints): pivot test of in.

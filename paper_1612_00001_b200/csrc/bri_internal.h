@@ -126,6 +126,10 @@ cudaError_t launch_diag_check(const ArenaView& a, const int* slots, int count,
 int trsm_smem_bytes();
 cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool lower, double* dinv,
                         int blk0, int nblocks, cudaStream_t s);
+// general triangle kind: lower/upper x unit/non-unit diagonal (transposed factors: Uᵀ is
+// lower non-unit, Lᵀ upper unit)
+cudaError_t launch_dinv_t(const ArenaView& a, const int* fslots, int count, bool lower, bool unit, double* dinv,
+                          int blk0, int nblocks, cudaStream_t s);
 // X * U[J0:J0+W, J0:J0+W] = B in place on columns [J0, J0 + W) of G, all rows;
 // gf: device (G, F) pairs; dinv_u: inverted upper diagonal blocks of F
 cudaError_t launch_rtrsm(const ArenaView& a, const int* gf, int count, const double* dinv_u, int J0, int W,

@@ -677,6 +677,29 @@ __global__ void transpose_kernel(ArenaView a, const int* items) {
   }
 }
 
+// dst(i, pi[x]) = src(x, i) in X-world (items: (src, dst) pairs, fidx: factor index of
+// each item's permutation): the last step of a right-side solve C = rt p^-1 computed
+// as its transpose (C^T = P (L^T)^-1 (U^T)^-1 rt^T) — transpose back and apply P, in one
+// pass; reads and writes stay coalesced through a 32 x 32 smem tile.
+__global__ void transpose_permute_kernel(ArenaView a, const int* items, const int* pi, int pi_stride,
+                                         const int* fidx) {
+  __shared__ double tile[32][33];
+  const int* it = items + 2 * blockIdx.z;
+  const double* src = a.base + (long long)it[0] * a.slot_elems;
+  double* dst = a.base + (long long)it[1] * a.slot_elems;
+  const int* p = pi + (long long)fidx[blockIdx.z] * pi_stride;
+  const int x0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // src(x, i): x contiguous for fixed i
+    const int x = x0 + threadIdx.x, i = i0 + r;
+    if (x < a.n && i < a.n) tile[r][threadIdx.x] = src[x + (long long)i * a.ld];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {   // dst(i, pi[x]): i contiguous for fixed x
+    const int i = i0 + threadIdx.x, x = x0 + r;
+    if (x < a.n && i < a.n) dst[i + (long long)p[x] * a.ld] = tile[threadIdx.x][r];
+  }
+}
+
 // Copy row-major blocks M[i*n : (i+1)*n, j*n : (j+1)*n] of a dense row-major
 // matrix (leading dim ldm) into arena slots.  items: (block row i, block col j,
 // slot), 0-based.  Arena slots hold the row-major block bytes (ld stride).
@@ -1162,29 +1185,50 @@ int bri_schur_batch_gated(bri_arena* ar, void* stream, int count, const int* ite
 // every node only pays its own fused GEMM-subtract.  Same kernels, same
 // operand bytes: each W and out is bit-identical to bri_schur_batch's large-
 // batch (unfolded) path.
-int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
-                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr);
+int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                       int nt, const int* titems, int nr, const int* ritems, int ng, const int* gitems, int* fstatus,
+                       void* ev_l, void* ev_rtr);
 
 int bri_level_batch(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems, int ng,
                     const int* gitems, int* fstatus) {
-  return bri_level_batch_gated(ar, stream, nf, fitems, ns, sitems, ng, gitems, fstatus, nullptr, nullptr);
+  return bri_level_batch_ex(ar, stream, nf, fitems, ns, sitems, 0, nullptr, 0, nullptr, ng, gitems, fstatus,
+                            nullptr, nullptr);
+}
+
+int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr) {
+  return bri_level_batch_ex(ar, stream, nf, fitems, ns, sitems, 0, nullptr, 0, nullptr, ng, gitems, fstatus,
+                            ev_l, ev_rtr);
 }
 
 // ev_l / ev_rtr (optional): the l operands / the rt and r operands are still
 // being copied in (first level of a run from pinned host memory); the solves
 // wait on ev_l, the GEMM-subtracts on ev_rtr, through external event nodes of
 // the captured graph (the caller re-records the same persistent events).
-int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
-                          int ng, const int* gitems, int* fstatus, void* ev_l, void* ev_rtr) {
+// Right-side solves (nr > 0): for pivots whose nodes share fewer distinct rt than l
+// operands, C = rt^ p^-1 is solved once per distinct (pivot, rt) and the nodes compute
+// out = r - C * l (the reference's own association, (rt inv(p)) l in X-world) instead of
+// out = r - rt * (p^-1 l).  Through transposes, with the left-side kernels:
+//   Ft = F^T (per factor, titems (fidx, Ft)): its lower part is U^T (non-unit), upper L^T (unit);
+//   S = rt^T;  S <- (U^T)^-1 S;  S <- (L^T)^-1 S;  C(i, pi[x]) = S(x, i)   (C^T = P S)
+// ritems: (tidx, rt, S, C), tidx indexing titems.
+int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, int ns, const int* sitems,
+                       int nt, const int* titems, int nr, const int* ritems, int ng, const int* gitems, int* fstatus,
+                       void* ev_l, void* ev_rtr) {
   BRI_NVTX("bri_level_batch");
-  if (ar == nullptr || nf < 0 || ns < 0 || ng < 0 || (nf && !fitems) || (ns && !sitems) || (ng && !gitems))
+  if (ar == nullptr || nf < 0 || ns < 0 || ng < 0 || nt < 0 || nr < 0 || (nf && !fitems) || (ns && !sitems) ||
+      (ng && !gitems) || (nt && !titems) || (nr && !ritems))
     return fail_msg("bri_level_batch: bad arguments");
-  if (nf == 0 && ns == 0 && ng == 0) return 0;
+  if (nf == 0 && ns == 0 && ng == 0 && nr == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = ar->v.n;
   if (n <= SMALL_MAX) return fail_msg("bri_level_batch: order <= SMALL_MAX uses bri_schur_batch");
   for (int i = 0; i < ns; ++i)
     if (sitems[3 * i] < 0 || sitems[3 * i] >= nf) return fail_msg("bri_level_batch: solve names a bad factor");
+  for (int i = 0; i < nt; ++i)
+    if (titems[2 * i] < 0 || titems[2 * i] >= nf) return fail_msg("bri_level_batch: transpose names a bad factor");
+  for (int i = 0; i < nr; ++i)
+    if (ritems[4 * i] < 0 || ritems[4 * i] >= nt) return fail_msg("bri_level_batch: right solve names a bad factor");
   // layout: [F (nf) | (p,F) (nf) | (F,F,F,F) (nf) | (F,F) (nf) | (l,W) (ns) | F_s (ns) | (F_s,W) (ns) |
   //          (F_s,W,W,W) (ns) | fidx (ns) | (rt,W,r,out) (ng)]
   std::vector<int> h;
@@ -1203,8 +1247,28 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
   }
   for (int i = 0; i < ns; ++i) h.push_back(sitems[3 * i]);
   for (int g = 0; g < 4 * ng; ++g) h.push_back(gitems[g]);
+  // right side: [(F,Ft) (nt) | (rt,S) (nr) | Ft_r (nr) | (Ft_r,S) (nr) | (Ft_r,S,S,S) (nr) | (S,C) (nr) | fidx_r (nr)]
+  const size_t r_base = h.size();
+  auto Ft = [&](int i) { return titems[2 * ritems[4 * i] + 1]; };
+  for (int t = 0; t < nt; ++t) { h.push_back(F(titems[2 * t])); h.push_back(titems[2 * t + 1]); }
+  for (int i = 0; i < nr; ++i) { h.push_back(ritems[4 * i + 1]); h.push_back(ritems[4 * i + 2]); }
+  for (int i = 0; i < nr; ++i) h.push_back(Ft(i));
+  for (int i = 0; i < nr; ++i) { h.push_back(Ft(i)); h.push_back(ritems[4 * i + 2]); }
+  for (int i = 0; i < nr; ++i) {
+    h.push_back(Ft(i));
+    for (int q = 0; q < 3; ++q) h.push_back(ritems[4 * i + 2]);
+  }
+  for (int i = 0; i < nr; ++i) { h.push_back(ritems[4 * i + 2]); h.push_back(ritems[4 * i + 3]); }
+  for (int i = 0; i < nr; ++i) h.push_back(titems[2 * ritems[4 * i]]);
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_tt = dev + r_base;
+  const int* d_rs = d_tt + 2 * (size_t)nt;
+  const int* d_rft = d_rs + 2 * (size_t)nr;
+  const int* d_rfs = d_rft + nr;
+  const int* d_rfsss = d_rfs + 2 * (size_t)nr;
+  const int* d_rsc = d_rfsss + 4 * (size_t)nr;
+  const int* d_rfidx = d_rsc + 2 * (size_t)nr;
   const int* d_f = dev;
   const int* d_pf = dev + nf;
   const int* d_ffff = dev + 3 * (size_t)nf;
@@ -1217,8 +1281,13 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
   const int* d_g = d_fidx + ns;
   LuLayout L = lu_layout(n, nf > 0 ? nf : 1);
   if (int rc = ar->ctx->lu.ensure(L.total, s)) return rc;
-  if (int rc = ensure_dinv(ar, s, nf > ns ? nf : ns)) return rc;
+  {
+    int most = nf > ns ? nf : ns;
+    if (nr > most) most = nr;
+    if (int rc = ensure_dinv(ar, s, most)) return rc;
+  }
   LuScratch sc = lu_scratch(ar->ctx->lu.ptr, L);
+  const size_t per_dinv = (size_t)((n + TRSM_BLOCK - 1) / TRSM_BLOCK) * TRSM_BLOCK * TRSM_BLOCK;
   auto issue = [&](cudaStream_t st) -> int {
     if (nf > 0) {
       BRI_CHECK(launch_copy(ar->v, d_pf, nf, st));
@@ -1229,6 +1298,26 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
       BRI_CHECK(launch_permcopy(ar->v, d_lw, ns, sc.pi, n, false, st, d_fidx));
       if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false, 1)) return rc;
     }
+    if (nr > 0) {   // C = rt^ p^-1 through the transposed factor (the dinv tables reuse the
+                    // region the left-side sweeps used: same stream, strictly after them)
+      const int tb = (n + 31) / 32;
+      count_launch();
+      transpose_kernel<<<dim3(tb, tb, nt), dim3(32, 8), 0, st>>>(ar->v, d_tt);
+      BRI_CHECK(cudaGetLastError());
+      if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
+      count_launch();
+      transpose_kernel<<<dim3(tb, tb, nr), dim3(32, 8), 0, st>>>(ar->v, d_rs);
+      BRI_CHECK(cudaGetLastError());
+      double* tl = static_cast<double*>(ar->ctx->dinv.ptr);
+      double* tu = tl + per_dinv * nr;
+      BRI_CHECK(launch_dinv_t(ar->v, d_rft, nr, true, false, tl, 0, 0, st));    // U^T: lower, non-unit
+      BRI_CHECK(launch_dinv_t(ar->v, d_rft, nr, false, true, tu, 0, 0, st));    // L^T: upper, unit
+      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, true, 0, n, n, tl)) return rc;
+      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, false, 0, n, n, tu)) return rc;
+      count_launch();
+      transpose_permute_kernel<<<dim3(tb, tb, nr), dim3(32, 8), 0, st>>>(ar->v, d_rsc, sc.pi, n, d_rfidx);
+      BRI_CHECK(cudaGetLastError());
+    }
     if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
     if (ev_rtr) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_rtr), cudaEventWaitExternal));
     if (ng > 0) return gemm_call(ar, st, d_g, ng, n, n, n, 0, 0, 0, 0, 0, 0, -1.0, 1.0, 0, 1);
@@ -1237,6 +1326,8 @@ int bri_level_batch_gated(bri_arena* ar, void* stream, int nf, const int* fitems
   std::vector<uintptr_t> key = graph_key(2, ar, ng, dev);
   key.push_back((uintptr_t)nf);
   key.push_back((uintptr_t)ns);
+  key.push_back((uintptr_t)nt);
+  key.push_back((uintptr_t)nr);
   key.push_back((uintptr_t)ev_l);
   key.push_back((uintptr_t)ev_rtr);
   if (int rc = run_graphed(ar->ctx, s, key, issue)) return rc;

@@ -46,6 +46,15 @@ namespace {
 template <int N>
 constexpr int sn_warps() { return N > 64 ? 16 : 8; }
 
+// named barriers (ids 1, 2; 0 is __syncthreads): the producer warp of a step arrives,
+// the others sync — the producer does not wait for its own publication
+BRI_DEVI void bar_arrive(int id, int nthreads) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+BRI_DEVI void bar_sync(int id, int nthreads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 BRI_DEVI void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -208,11 +217,17 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
 #pragma unroll
     for (int h = 0; h < R; ++h) A[h][q] = fma(-lm[h], u, A[h][q]);   // l = 0: unchanged
   };
-  if (warp == 0 && n > 0) pivot_step(0, 0);
+  // make the max |p| reduction and the zeroed smem visible before the sweep
+  __syncthreads();
+  if (warp == 0 && n > 0) {
+    pivot_step(0, 0);
+    bar_arrive(1, SN_THREADS);
+  }
   // qj (the register column of j) must be a compile-time index: unrolled outer loop over
   // register columns, rolled inner loop over the warps that own them.  Lookahead: the
-  // owner of column j+1 updates that column first and publishes step j+1's pivot before
-  // its other columns, so the pivot search leaves the critical path of the update.
+  // owner of column j+1 updates that column first, publishes step j+1's pivot and ARRIVES
+  // at that step's named barrier (ids alternate 1 / 2) before its other columns; the other
+  // warps sync on it.  The critical path per column is one pivot search, not a full update.
 #pragma unroll
   for (int qj = 0; qj < N / NW; ++qj)
 #pragma unroll 1
@@ -220,7 +235,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     const int j = qj * NW + wj;
     if (j >= n) break;
     const int buf = j & 1;
-    __syncthreads();
+    if (warp != wj) bar_sync(1 + buf, SN_THREADS);   // the owner of column j published it
     const int rp = prow_s[buf], pp = ppos_s[buf];
     const int srcl = rp & 31, hp = rp >> 5;
     double lm[R];
@@ -241,6 +256,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
         update_col(qj + 1, lm, srcl, hp);
         pivot_step(j + 1, qj + 1);
       }
+      bar_arrive(1 + ((j + 1) & 1), SN_THREADS);
     }
     // rank-1 update of the trailing matrix and the forward sweep of the right-hand side
     // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order); register

@@ -54,7 +54,9 @@ BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
 constexpr int DINV_WARPS = 8;
 constexpr int DINV_COLS = T / DINV_WARPS;   // columns per warp
 
-template <bool LOWER>
+// UNIT: the triangle's diagonal is taken as 1 (LU's L, or the Lᵀ of a transposed factor);
+// otherwise its stored diagonal is used (U, or the Uᵀ of a transposed factor).
+template <bool LOWER, bool UNIT = LOWER>
 __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
                                                                int nblk, int blk0) {
   __shared__ double S[T][T + 1];   // S[c][r] = block(r, c)
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
     const int r = e % T, cc = e / T;
     const int gi = base + r, gj = base + cc;
     double v = (gi < a.n && gj < a.n) ? F[gi + (long long)gj * a.ld] : (r == cc ? 1.0 : 0.0);
-    if (LOWER && r == cc) v = 1.0;
+    if (UNIT && r == cc) v = 1.0;
     if (LOWER && r < cc) v = 0.0;
     if (!LOWER && r > cc) v = 0.0;
     S[cc][r] = v;
@@ -81,13 +83,29 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
   }
   if (LOWER) {
 #pragma unroll 2
-    for (int k = 0; k < T - 1; ++k) {
+    for (int k = 0; k < T; ++k) {
+      const double s0 = S[k][lane], s1 = S[k][lane + 32];
+#pragma unroll
+      for (int q = 0; q < DINV_COLS; ++q) {
+        if (!UNIT) {   // x_k /= l_kk before it propagates (forward substitution, non-unit)
+          const double dk = S[k][k];
+          if (k >= 32) { if (lane == k - 32) x1[q] /= dk; } else { if (lane == k) x0[q] /= dk; }
+        }
+        if (UNIT && k == T - 1) continue;
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
+        if (lane > k) x0[q] = fma(-s0, xk, x0[q]);
+        if (lane + 32 > k) x1[q] = fma(-s1, xk, x1[q]);
+      }
+    }
+  } else if (UNIT) {   // unit upper (Lᵀ): backward substitution without divisions
+#pragma unroll 2
+    for (int k = T - 1; k >= 0; --k) {
       const double s0 = S[k][lane], s1 = S[k][lane + 32];
 #pragma unroll
       for (int q = 0; q < DINV_COLS; ++q) {
         const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
-        if (lane > k) x0[q] = fma(-s0, xk, x0[q]);
-        if (lane + 32 > k) x1[q] = fma(-s1, xk, x1[q]);
+        if (lane < k) x0[q] = fma(-s0, xk, x0[q]);
+        if (lane + 32 < k) x1[q] = fma(-s1, xk, x1[q]);
       }
     }
   } else {
@@ -417,6 +435,20 @@ cudaError_t launch_rtrsm(const ArenaView& a, const int* gf, int count, const dou
   p.W = W;
   count_launch();
   rtrsm_kernel<<<dim3((a.n + RT_R - 1) / RT_R, count), RT_THREADS, RT_SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dinv_t(const ArenaView& a, const int* fslots, int count, bool lower, bool unit, double* dinv,
+                          int blk0, int nblocks, cudaStream_t s) {
+  if (lower == unit) return launch_dinv(a, fslots, count, lower, dinv, blk0, nblocks, s);
+  const int nblk = (a.n + T - 1) / T;
+  if (nblocks <= 0) nblocks = nblk - blk0;
+  dim3 grid(nblocks, count);
+  count_launch();
+  if (lower)
+    dinv_kernel<true, false><<<grid, DINV_WARPS * 32, 0, s>>>(a, fslots, dinv, nblk, blk0);
+  else
+    dinv_kernel<false, true><<<grid, DINV_WARPS * 32, 0, s>>>(a, fslots, dinv, nblk, blk0);
   return cudaGetLastError();
 }
 

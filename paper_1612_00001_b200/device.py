@@ -157,16 +157,19 @@ class Arena:
         _native.check(self.lib.bri_schur_batch(self.handle, self.stream, len(items), self._items(flat),
                                                ctypes.c_void_p(status.data_ptr())), "bri_schur_batch")
 
-    def level(self, fitems, sitems, gitems, fstatus, ev_l=None, ev_rtr=None) -> None:
-        """One DAG level with shared work (bri_level_batch): fitems (p, F) factor each distinct
-        pivot once, sitems (factor index, l, W) solve each distinct (pivot, l) once, gitems
-        (rt, W, r, out) one fused GEMM-subtract per node; fstatus: int32 device tensor (nf).
+    def level(self, fitems, sitems, gitems, fstatus, ev_l=None, ev_rtr=None, titems=(), ritems=()) -> None:
+        """One DAG level with shared work (bri_level_batch_ex): fitems (p, F) factor each distinct
+        pivot once, sitems (factor index, l, W) solve each distinct (pivot, l) once, titems
+        (factor index, Ft) / ritems (titem index, rt, S, C) solve C = rt p^-1 once per distinct
+        (pivot, rt) for pivots solved from the right, gitems (A, B, r, out) one fused
+        GEMM-subtract per node ((rt, W, ...) or (C, l, ...)); fstatus: int32 device tensor (nf).
         ev_l / ev_rtr: torch.cuda.Events the solves / GEMMs wait on (operands in flight)."""
         arr = lambda items: self._items([s for it in items for s in it]) if items else None
         h = lambda ev: ctypes.c_void_p(ev.cuda_event) if ev is not None else None
-        _native.check(self.lib.bri_level_batch_gated(self.handle, self.stream, len(fitems), arr(fitems), len(sitems),
-                                                     arr(sitems), len(gitems), arr(gitems),
-                                                     ctypes.c_void_p(fstatus.data_ptr()), h(ev_l), h(ev_rtr)),
+        _native.check(self.lib.bri_level_batch_ex(self.handle, self.stream, len(fitems), arr(fitems), len(sitems),
+                                                  arr(sitems), len(titems), arr(titems), len(ritems), arr(ritems),
+                                                  len(gitems), arr(gitems), ctypes.c_void_p(fstatus.data_ptr()),
+                                                  h(ev_l), h(ev_rtr)),
                       "bri_level_batch")
 
     def schur_gated(self, items, status, ev_l, ev_rtr) -> None:

@@ -252,8 +252,11 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
     if base_need + 3 > max_slots:
         raise _TooBig(f"DAG needs {base_need} resident blocks of order {b} but the arena budget holds "
                       f"{max_slots}; raise Workspace(arena_bytes=...) or use schedule='tree'")
-    chunk = max(1, min(width, (max_slots - base_need) // 2, 65535))
-    nslots = min(max_slots, base_need + 2 * chunk + 1)
+    # scratch per node of a chunk: factor + W (left-side solves), or factor + transposed
+    # factor + S + C (right-side solves, b > SMALL_MAX)
+    per = 4 if (b > SMALL_MAX and _SOLVE_SIDE != "l") else 2
+    chunk = max(1, min(width, (max_slots - base_need) // per, 65535))
+    nslots = min(max_slots, base_need + per * chunk + 1)
     info = RunInfo("dag", nroots, len(sched.nodes), sum(sched.tree_nodes(t) for t in range(nroots)),
                    {n: len(v) for n, v in levels.items()}, nslots, chunk)
     # one status tensor (nodes, then roots): one fill, one device -> host read
@@ -300,9 +303,12 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                 slot_of = lambda r: mslot[(r[1], r[2])] if r[0] == "m" else val[r[1]]
                 scratch = []
                 if b > SMALL_MAX and len(part) > 2:
-                    # shared work: one factorization per distinct pivot, one solve per
-                    # distinct (pivot, l), one fused GEMM-subtract per node
-                    fidx, sidx, fitems, sitems, gitems = {}, {}, [], [], []
+                    # shared work: one factorization per distinct pivot; per pivot, one solve
+                    # per distinct l (W = p^-1 l, out = r - rt W) or — when its nodes share
+                    # fewer distinct rt than l — per distinct rt (C = rt p^-1, out = r - C l);
+                    # one fused GEMM-subtract per node
+                    sides = _solve_sides(sched, part)
+                    fidx, sidx, tidx, fitems, sitems, titems, ritems, gitems = {}, {}, {}, [], [], [], [], []
                     for nid in part:
                         refs = sched.nodes[nid].operands
                         if refs[0] not in fidx:
@@ -310,33 +316,51 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                             fidx[refs[0]] = len(fitems)
                             fitems.append((slot_of(refs[0]), f))
                             scratch.append(f)
-                        sk = (refs[0], refs[2])
-                        if sk not in sidx:
-                            w = arena.alloc()
-                            sidx[sk] = w
-                            sitems.append((fidx[refs[0]], slot_of(refs[2]), w))
-                            scratch.append(w)
                         out = arena.alloc()
-                        gitems.append((slot_of(refs[1]), sidx[sk], slot_of(refs[3]), out))
+                        if sides[refs[0]] == "l":
+                            sk = ("l", refs[0], refs[2])
+                            if sk not in sidx:
+                                w = arena.alloc()
+                                sidx[sk] = w
+                                sitems.append((fidx[refs[0]], slot_of(refs[2]), w))
+                                scratch.append(w)
+                            gitems.append((slot_of(refs[1]), sidx[sk], slot_of(refs[3]), out))
+                        else:
+                            if refs[0] not in tidx:
+                                ft = arena.alloc()
+                                tidx[refs[0]] = len(titems)
+                                titems.append((fidx[refs[0]], ft))
+                                scratch.append(ft)
+                            sk = ("rt", refs[0], refs[1])
+                            if sk not in sidx:
+                                s_, c_ = arena.alloc(), arena.alloc()
+                                sidx[sk] = c_
+                                ritems.append((tidx[refs[0]], slot_of(refs[1]), s_, c_))
+                                scratch += (s_, c_)
+                            gitems.append((sidx[sk], slot_of(refs[2]), slot_of(refs[3]), out))
                         val[nid] = out
                         pos[nid] = pbase + fidx[refs[0]]
-                    if gates is not None:   # first level from pinned host: l, rt, r may be in flight
-                        arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)], *gates)
-                        gates = None
-                    else:
-                        arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)])
+                    lv_gates = gates if gates is not None else (None, None)
+                    gates = None    # first level from pinned host: l, rt, r may still be in flight
+                    arena.level(fitems, sitems, gitems, status[pbase:pbase + len(fitems)], *lv_gates,
+                                titems=titems, ritems=ritems)
                     pbase += len(fitems)
                     info.factorizations += len(fitems)
-                    info.solves += len(sitems)
+                    info.solves += len(sitems) + len(ritems)
                 else:
                     items = []
+                    small = b <= SMALL_MAX   # the one-CTA node kernel keeps its factor in registers
                     for nid in part:
                         ops = [slot_of(r) for r in sched.nodes[nid].operands]
-                        out, f, w = arena.alloc(), arena.alloc(), arena.alloc()
+                        out = arena.alloc()
+                        if small:
+                            f = w = out
+                        else:
+                            f, w = arena.alloc(), arena.alloc()
+                            scratch += (f, w)
                         items.append((ops[0], ops[1], ops[2], ops[3], out, f, w))
                         val[nid] = out
                         pos[nid] = pbase + len(items) - 1
-                        scratch += (f, w)
                     if gates is not None:
                         arena.schur_gated(items, status[pbase:pbase + len(part)], *gates)
                         gates = None
@@ -395,6 +419,23 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
         arena.release_all()
     sched.first_failure(pstat, rstat, b)
     return results, info
+
+
+_SOLVE_SIDE = os.environ.get("BRI_SOLVE_SIDE", "auto")   # "auto" | "l" (always W = p^-1 l)
+
+
+def _solve_sides(sched, part) -> dict:
+    """Per distinct pivot of a level chunk: "l" (solve W = p^-1 l per distinct l) or "rt"
+    (solve C = rt p^-1 per distinct rt), whichever needs fewer solves (ties: "l").
+    Config 3: 3,902 -> 3,204 solves; config 4: 22,224 -> 18,012."""
+    ls, rts = {}, {}
+    for nid in part:
+        refs = sched.nodes[nid].operands
+        ls.setdefault(refs[0], set()).add(refs[2])
+        rts.setdefault(refs[0], set()).add(refs[1])
+    if _SOLVE_SIDE == "l":
+        return {p: "l" for p in ls}
+    return {p: ("rt" if len(rts[p]) < len(ls[p]) else "l") for p in ls}
 
 
 def _gather_slots(arena, slots):
