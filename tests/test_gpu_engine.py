@@ -194,11 +194,16 @@ def test_config2_full_size(bri):
     assert _rel(out, x_col) <= 1e-9
 
 
-def test_bounded_arena_groups_targets():
+def test_bounded_arena_groups_targets(monkeypatch):
     """A DAG that does not fit the arena budget is split into target groups
     (engine._run_grouped); results equal the unbounded run bit for bit, the
     device footprint stays under the budget, and a single target that cannot
-    fit runs the bounded-footprint schedule instead."""
+    fit runs the bounded-footprint schedule instead.  (Bitwise with left-side
+    solves: which side a pivot is solved from depends on the nodes that share it,
+    so grouping can change it — and with it the rounding.)"""
+    from paper_1612_00001_b200 import engine
+
+    monkeypatch.setattr(engine, "_SOLVE_SIDE", "l")
     import torch
 
     import paper_1612_00001_b200 as bri
@@ -257,9 +262,13 @@ def test_bounded_schedule_spills_bitwise(bri, b, budget):
         bri.invert_blocks(prov, [(1, 1)], bri.Workspace(arena_bytes=budget * b * ld * 8, host_bytes=b * ld * 8))
 
 
-def test_bounded_schedule_many_targets_and_reduce_frame(bri):
+def test_bounded_schedule_many_targets_and_reduce_frame(bri, monkeypatch):
     """schedule='bounded' over several targets (roots inverted as soon as they exist) and
-    through reduce_frame (un-inverted roots) equals the DAG run bit for bit."""
+    through reduce_frame (un-inverted roots) equals the DAG run bit for bit (both with
+    left-side solves: the bounded schedule runs one node at a time)."""
+    from paper_1612_00001_b200 import engine
+
+    monkeypatch.setattr(engine, "_SOLVE_SIDE", "l")
     import torch
 
     a = shifted(6 * 104, 43)
@@ -277,11 +286,14 @@ def test_bounded_schedule_many_targets_and_reduce_frame(bri):
     np.testing.assert_array_equal(r1, r2)
 
 
-def test_node_sharded_device_executor_world1(bri, golden):
+def test_node_sharded_device_executor_world1(bri, golden, monkeypatch):
     """invert_blocks_sharded on the device executor (NCCL process group of one rank: the
     exchange is empty, the arena executor, status replay and root hand-off are exercised);
-    blocks equal the single-process DAG run bit for bit.  The multi-rank exchange itself is
-    covered on CPU (tests/test_multiproc.py, gloo)."""
+    blocks equal the single-process DAG run (left-side solves) bit for bit.  The multi-rank
+    exchange itself is covered on CPU (tests/test_multiproc.py, gloo)."""
+    from paper_1612_00001_b200 import engine
+
+    monkeypatch.setattr(engine, "_SOLVE_SIDE", "l")
     import socket
 
     import torch
