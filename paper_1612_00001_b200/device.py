@@ -101,6 +101,15 @@ class Arena:
         self.handle = handle
         self._free = list(range(nslots - 1, -1, -1))
         self._live = set()
+        self.recorder = None   # list: C-ABI calls of a run are recorded for replay (engine run programs)
+        self.max_live = 0
+
+    def _call(self, name: str, *args) -> None:
+        """Issue one C-ABI entry point (and record it when a run program is being built)."""
+        fn = getattr(self.lib, name)
+        _native.check(fn(*args), name)
+        if self.recorder is not None:
+            self.recorder.append((fn, args, name))
 
     # ------------------------------------------------------------ slots
     def alloc(self) -> int:
@@ -108,6 +117,8 @@ class Arena:
             raise BadPartitionError(f"arena exhausted ({self.nslots} blocks of order {self.n})")
         s = self._free.pop()
         self._live.add(s)
+        if len(self._live) > self.max_live:
+            self.max_live = len(self._live)
         if self.gauge is not None:
             self.gauge.on_alloc()
         return s
@@ -154,8 +165,8 @@ class Arena:
     def schur(self, items, status) -> None:
         """items: list of (p, rt, l, r, out, f, w) slot tuples; status: int32 device tensor."""
         flat = [s for it in items for s in it]
-        _native.check(self.lib.bri_schur_batch(self.handle, self.stream, len(items), self._items(flat),
-                                               ctypes.c_void_p(status.data_ptr())), "bri_schur_batch")
+        self._call("bri_schur_batch", self.handle, self.stream, len(items), self._items(flat),
+                   ctypes.c_void_p(status.data_ptr()))
 
     def level(self, fitems, sitems, gitems, fstatus, ev_l=None, ev_rtr=None, titems=(), ritems=()) -> None:
         """One DAG level with shared work (bri_level_batch_ex): fitems (p, F) factor each distinct
@@ -191,8 +202,8 @@ class Arena:
     def invert(self, items, status) -> None:
         """items: list of (in, f, out)."""
         flat = [s for it in items for s in it]
-        _native.check(self.lib.bri_invert_batch(self.handle, self.stream, len(items), self._items(flat),
-                                                ctypes.c_void_p(status.data_ptr())), "bri_invert_batch")
+        self._call("bri_invert_batch", self.handle, self.stream, len(items), self._items(flat),
+                   ctypes.c_void_p(status.data_ptr()))
 
     def getrf(self, slots, perm, status, ipiv=None) -> None:
         _native.check(self.lib.bri_getrf_batch(
@@ -225,9 +236,8 @@ class Arena:
     def gather(self, matrix, items) -> None:
         """Copy blocks of a device row-major matrix: items (block row, block col, slot), 0-based."""
         flat = [s for it in items for s in it]
-        _native.check(self.lib.bri_gather_blocks(self.handle, self.stream, ctypes.c_void_p(matrix.data_ptr()),
-                                                 matrix.stride(0), len(items), self._items(flat)),
-                      "bri_gather_blocks")
+        self._call("bri_gather_blocks", self.handle, self.stream, ctypes.c_void_p(matrix.data_ptr()),
+                   matrix.stride(0), len(items), self._items(flat))
 
     def gather_elements(self, matrix, m, rmap, cmap, items) -> None:
         """Padded-view gather: items (block row, block col, slot); rmap/cmap int32 device tensors."""

@@ -41,6 +41,7 @@ import numpy as np
 
 from .core import Block, Workspace
 from .dag import build_from_specs, build_schedule, target_maps
+from . import _native
 from .device import SMALL_MAX, Arena, cached_arena, cached_bytes, current_device, free_bytes, padded_ld
 from .errors import (BadPartitionError, DimensionMismatchError, IndexOutOfRangeError,
                      SingularBlockError, SingularPivotError)
@@ -261,10 +262,25 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                    {n: len(v) for n, v in levels.items()}, nslots, chunk)
     # one status tensor (nodes, then roots): one fill, one device -> host read
     nst = max(1, len(sched.nodes))
+    # small orders: the whole run is a handful of C-ABI calls whose arguments depend only on
+    # the schedule, the matrix and the arena — replay the recorded calls (run programs)
+    pkey = None
+    if trace is None and b <= SMALL_MAX and isinstance(src, _DeviceSource):
+        pkey = (id(sched), b, device, bool(invert_roots), nslots, chunk, src.matrix.data_ptr(),
+                src.matrix.stride(0), threading.get_ident())
+        prog = _PROGRAMS.get(pkey)
+        if prog is not None and prog.sched is sched:
+            arena = cached_arena(b, nslots, device, gauge=ws.gauge)
+            if arena is prog.arena and arena.handle.value == prog.handle:
+                return _replay(prog, arena, sched, ws, info, invert_roots)
+            _PROGRAMS.pop(pkey, None)
     st_all = torch.zeros(nst + max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
     status, root_status = st_all[:nst], st_all[nst:]
     results = []
     arena = cached_arena(b, nslots, device, gauge=ws.gauge)
+    out_slots = []
+    if pkey is not None:
+        arena.recorder, arena.max_live = [], 0
     try:
         mslot = {}
         for ij in used:
@@ -391,12 +407,14 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                     outs.append((f, out))
                 arena.invert(items, root_status[t0:t0 + len(part)])
                 # one gather for the whole chunk (the blocks are views of one result tensor)
-                results += _gather_slots(arena, [out for _, out in outs])
+                out_slots.append([out for _, out in outs])
+                results += _gather_slots(arena, out_slots[-1])
                 for f, out in outs:
                     arena.release(f)
                     arena.release(out)
         else:
-            results += _gather_slots(arena, [val[sched.roots[t]] for t in range(nroots)])
+            out_slots.append([val[sched.roots[t]] for t in range(nroots)])
+            results += _gather_slots(arena, out_slots[-1])
         st_host = st_all.cpu().numpy()  # synchronizes the stream
         node_status = st_host[: len(sched.nodes)]
         rstat = st_host[nst:nst + nroots] if invert_roots else None
@@ -415,10 +433,60 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
             for t in range(nroots):
                 sched.walk(t, on_node=on_node)
         info.peak_blocks = ws.gauge.peak_blocks
+        if pkey is not None and len(arena.recorder) <= 64:
+            pos_arr = np.zeros(len(sched.nodes), dtype=np.int64)
+            for nid, p_ in pos.items():
+                pos_arr[nid] = p_
+            _PROGRAMS[pkey] = _RunProgram(sched, arena, arena.handle.value, list(arena.recorder), out_slots,
+                                          st_all, pos_arr, nst, arena.max_live, info)
+            if len(_PROGRAMS) > 32:
+                _PROGRAMS.pop(next(iter(_PROGRAMS)))
     finally:
+        arena.recorder = None
         arena.release_all()
     sched.first_failure(pstat, rstat, b)
     return results, info
+
+
+@dataclass
+class _RunProgram:
+    """The C-ABI calls of one small-order DAG run, replayed when the same schedule runs again on the
+    same matrix and arena: no Python item building, no slot bookkeeping (the gauge still sees the
+    run's peak), one status read."""
+
+    sched: object
+    arena: object
+    handle: int
+    calls: list           # (fn, args, name); args[1] (the stream) is substituted at replay
+    out_slots: list       # per root chunk: the slots holding the results
+    st_all: object        # the status tensor the recorded calls write into
+    pos_arr: object       # node id -> position of its pivot status
+    nst: int
+    peak: int             # arena blocks live at the run's peak
+    info: RunInfo
+
+
+_PROGRAMS: "OrderedDict" = OrderedDict()
+
+
+def _replay(prog, arena, sched, ws, info, invert_roots):
+    stream = arena.stream
+    for fn, args, name in prog.calls:
+        _native.check(fn(args[0], stream, *args[2:]), name)
+    results = []
+    for slots in prog.out_slots:
+        results += _gather_slots(arena, slots)
+    st_host = prog.st_all.cpu().numpy()  # synchronizes the stream
+    pstat = st_host[: prog.nst][prog.pos_arr].astype(np.int64)
+    rstat = st_host[prog.nst:prog.nst + len(sched.specs)] if invert_roots else None
+    if ws.gauge is not None and prog.peak:
+        ws.gauge.on_alloc(prog.peak)
+        ws.gauge.on_release(prog.peak)
+    run = RunInfo(**{f: getattr(prog.info, f) for f in prog.info.__dataclass_fields__})
+    run.levels = dict(prog.info.levels)
+    run.peak_blocks = ws.gauge.peak_blocks if ws.gauge is not None else prog.peak
+    sched.first_failure(pstat, rstat, arena.n)
+    return results, run
 
 
 _SOLVE_SIDE = os.environ.get("BRI_SOLVE_SIDE", "auto")   # "auto" | "l" (always W = p^-1 l)
