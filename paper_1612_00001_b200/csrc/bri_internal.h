@@ -96,7 +96,16 @@ struct LuScratch {
   unsigned long long* scale_bits;  // 1 (max |X| as double bits)
   int* status;    // 1
   int* orig;      // n   (tall panels: original row now at each position)
+  int* snap;      // nob * n  (deferred interchanges: inverse of pi after each outer block)
 };
+
+// Deferred left-side interchanges of a blocked LU (lu.cu): snapshot pi's inverse after
+// outer block J; at the end put every L column of block J into the final row order with
+// one gather per column segment (instead of one laswp pass per later block).
+cudaError_t launch_pi_snapshot(const int* pi, int* snap, int n, int nob, int J, int count, cudaStream_t s);
+cudaError_t launch_laswp_deferred(const ArenaView& a, const int* slots, int count, const int* pi,
+                                  const int* snap, int nob, int outer, cudaStream_t s);
+int laswp_deferred_max_n();
 
 cudaError_t launch_maxabs(const ArenaView& a, const int* slots, int count,
                           unsigned long long* scale_bits, cudaStream_t s);

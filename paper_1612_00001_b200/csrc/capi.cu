@@ -166,7 +166,7 @@ int upload(bri_ctx* ctx, cudaStream_t s, const std::vector<int>& h, int** dev) {
 
 struct LuLayout {
   int n, count, npanels, pair_stride;
-  size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, off_orig, total;
+  size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, off_orig, off_snap, total;
 };
 
 LuLayout lu_layout(int n, int count) {
@@ -189,6 +189,7 @@ LuLayout lu_layout(int n, int count) {
   L.off_scale = take((size_t)count * 8);
   L.off_status = take((size_t)count * 4);
   L.off_orig = take((size_t)count * n * 4);
+  L.off_snap = n <= laswp_deferred_max_n() ? take((size_t)count * ((n + LU_OUTER - 1) / LU_OUTER) * n * 4) : off;
   L.total = off;
   return L;
 }
@@ -203,6 +204,7 @@ LuScratch lu_scratch(void* base, const LuLayout& L) {
   s.scale_bits = reinterpret_cast<unsigned long long*>(b + L.off_scale);
   s.status = reinterpret_cast<int*>(b + L.off_status);
   s.orig = reinterpret_cast<int*>(b + L.off_orig);
+  s.snap = reinterpret_cast<int*>(b + L.off_snap);
   return s;
 }
 
@@ -408,7 +410,17 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(cudaStreamWaitEvent(s2, ctx->ev_d, 0));
     return fold_block(s2, J0, W, pidx0, npan);
   };
-  const int left = fold ? 0 : 1;   // 0: skip the interchanges of L left of the block
+  // Left-side interchanges (L columns of earlier blocks): applied per block (left = 1), skipped
+  // (the folded path never reads L, left = 0), or deferred — large batches snapshot pi after
+  // each block and reorder every L column once at the end (laswp_deferred; config 3 spent ~2%
+  // of its step in the per-block left passes).  Same values either way: only row order moves.
+  static const int defer_env = [] {
+    const char* e = getenv("BRI_DEFER_LASWP");
+    return e ? atoi(e) : 1;
+  }();
+  const bool defer_left = !fold && defer_env && vcount > 2 && n <= laswp_deferred_max_n() && n > LU_OUTER;
+  const int nob = (n + LU_OUTER - 1) / LU_OUTER;
+  const int left = (fold || defer_left) ? 0 : 1;   // 0: skip the interchanges of L left of the block
 
   const int npan_outer = outer / nbi;
   static const bool lookahead = [] {
@@ -428,6 +440,9 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   const int ext0 = extend ? (n < 2 * outer ? n : 2 * outer) : W0;
   if (int rc = factor_block(0, W0, 0, ext0, nullptr)) return rc;
   for (int J0 = 0, pidx0 = 0; J0 < n; J0 += outer, pidx0 += npan_outer) {
+    // block J's panels are done on s (its row permutation is final for rows < J0 + W)
+    if (defer_left && J0 + outer < n)
+      BRI_CHECK(launch_pi_snapshot(sc.pi, sc.snap, n, nob, J0 / outer, count, s));
     const int W = (n - J0) < outer ? (n - J0) : outer;
     const int npan = (W + nbi - 1) / nbi;
     const int N0 = J0 + W;
@@ -499,6 +514,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(cudaEventRecord(ctx->ev_w, s2));
     BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_w, 0));
   }
+  if (defer_left) BRI_CHECK(launch_laswp_deferred(v, dev_slots, count, sc.pi, sc.snap, nob, outer, s));
   BRI_CHECK(launch_diag_check(v, dev_slots, count, sc.scale_bits, sc.status, s));
   return 0;
 }

@@ -696,6 +696,40 @@ __global__ void __launch_bounds__(RP_THREADS) laswp_kernel(LaswpArgs p) {
   }
 }
 
+// ------------------------------------------------------------- deferred interchanges
+// snap[item][J][pi[x]] = x: where each original row sat after outer block J
+__global__ void pi_snapshot_kernel(const int* pi, int* snap, int n, int nob, int J) {
+  const int item = blockIdx.x;
+  const int* p = pi + (long long)item * n;
+  int* q = snap + ((long long)item * nob + J) * n;
+  for (int x = threadIdx.x; x < n; x += blockDim.x) q[p[x]] = x;
+}
+
+constexpr int LD_WARPS = 4;
+constexpr int LD_MAXN = 4096;   // a warp stages one column segment (< n doubles) in smem
+
+// L column c of outer block J (rows >= (J+1)*outer): final[x] = at_J[inv_J[pi[x]]] — the
+// interchanges of every later block at once, one warp per column.
+__global__ void __launch_bounds__(LD_WARPS * 32) laswp_deferred_kernel(ArenaView a, const int* slots,
+                                                                       const int* pi, const int* snap,
+                                                                       int nob, int outer, int ncols) {
+  extern __shared__ double seg_s[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * LD_WARPS + warp;
+  const int item = blockIdx.y;
+  if (c >= ncols) return;
+  const int n = a.n;
+  const int J = c / outer;
+  const int r0 = (J + 1) * outer;
+  double* col = a.base + (long long)slots[item] * a.slot_elems + (long long)c * a.ld;
+  const int* p = pi + (long long)item * n;
+  const int* inv = snap + ((long long)item * nob + J) * n;
+  double* seg = seg_s + (long long)warp * LD_MAXN;
+  for (int x = r0 + lane; x < n; x += 32) seg[x - r0] = col[x];
+  __syncwarp();
+  for (int x = r0 + lane; x < n; x += 32) col[x] = seg[inv[p[x]] - r0];
+}
+
 // ------------------------------------------------------------- diag check
 __global__ void diag_check_kernel(ArenaView a, const int* slots, const unsigned long long* scale_bits,
                                   int* status) {
@@ -805,6 +839,8 @@ cudaError_t configure_lu() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_tall_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(laswp_deferred_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LD_WARPS * LD_MAXN * 8);
   return e;
 }
 
@@ -929,6 +965,24 @@ cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0
   const int wpb = RP_THREADS / 32;
   count_launch();
   laswp_kernel<<<dim3((cols + wpb - 1) / wpb, count), RP_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+int laswp_deferred_max_n() { return LD_MAXN; }
+
+cudaError_t launch_pi_snapshot(const int* pi, int* snap, int n, int nob, int J, int count, cudaStream_t s) {
+  count_launch();
+  pi_snapshot_kernel<<<count, 256, 0, s>>>(pi, snap, n, nob, J);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_laswp_deferred(const ArenaView& a, const int* slots, int count, const int* pi,
+                                  const int* snap, int nob, int outer, cudaStream_t s) {
+  const int ncols = (nob - 1) * outer;   // the last block has no later interchanges
+  if (ncols <= 0) return cudaSuccess;
+  count_launch();
+  laswp_deferred_kernel<<<dim3((ncols + LD_WARPS - 1) / LD_WARPS, count), LD_WARPS * 32, LD_WARPS * LD_MAXN * 8,
+                          s>>>(a, slots, pi, snap, nob, outer, ncols);
   return cudaGetLastError();
 }
 

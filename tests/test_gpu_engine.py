@@ -329,3 +329,33 @@ def test_node_sharded_device_executor_world1(bri, golden, monkeypatch):
         assert [q.name for q in exc.value.path] == meta["singular"]["path"]
     finally:
         dist.destroy_process_group()
+
+
+def test_run_program_replay_small_order(bri, golden):
+    """Small-order DAG runs on an HBM-resident matrix replay their recorded C-ABI calls on repeat
+    (engine run programs): the replay returns the same bits, the gauge sees the same peak, the
+    counters advance the same way, and a singular pivot is reported again on replay."""
+    import torch
+
+    from paper_1612_00001_b200 import engine
+
+    a = torch.from_numpy(rng(0).uniform(-1.0, 1.0, (256, 256)) + 256 * np.eye(256)).cuda()
+    prov = bri.make_memory_provider(a, 4)
+    targets = [(al, be) for al in range(1, 5) for be in range(1, 5)]
+    ws1 = bri.Workspace()
+    first, i1 = bri.invert_blocks(prov, targets, ws1)
+    n_prog = len(engine._PROGRAMS)
+    ws2 = bri.Workspace()
+    second, i2 = bri.invert_blocks(prov, targets, ws2)
+    assert len(engine._PROGRAMS) == n_prog and n_prog >= 1
+    for x, y in zip(first, second):
+        assert torch.equal(x, y)
+    assert ws1.gauge.peak_blocks == ws2.gauge.peak_blocks and ws2.gauge.live_blocks == 0
+    assert ws1.counters == ws2.counters and ws1.executed == ws2.executed
+    assert (i1.dag_nodes, i1.levels) == (i2.dag_nodes, i2.levels)
+    data, meta = golden
+    sing = bri.make_memory_provider(torch.from_numpy(data["singular_matrix"]).cuda(), 3)
+    for _ in range(2):
+        with pytest.raises(bri.SingularPivotError) as exc:
+            bri.invert_blocks(sing, [(1, 1)])
+        assert [q.name for q in exc.value.path] == meta["singular"]["path"]

@@ -1,0 +1,33 @@
+#!/bin/bash
+# Round-end evidence on one B200 (one gpurun call): GPU test suite, bench lines (ours + reference
+# arm, configs 3 / 1 / 2), the ncu launch list of one config-3 step and `ncu --set full` captures of
+# the top kernels.  Each ncu pass runs only after the same command exited 0 without ncu.
+set -u
+OUT=gpurun_out/final
+mkdir -p $OUT
+python -m pytest tests -m gpu -q -p no:cacheprovider -rf > $OUT/gputest.log 2>&1; echo "rc=$?" >> $OUT/gputest.log
+python bench.py > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err; echo "rc=$?" >> $OUT/bench_cfg3.err
+python bench.py --impl reference > $OUT/ref_cfg3.json 2> $OUT/ref_cfg3.err
+python bench.py --config 1 > $OUT/bench_cfg1.json 2> $OUT/bench_cfg1.err
+python bench.py --config 2 > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err
+python tools/timeline.py --config 3 --out $OUT/timeline_cfg3.json > $OUT/timeline_cfg3.txt 2>&1
+# launch list: one config-3 step (cold-cache, serialised: compare shares, not absolutes)
+python tools/profile_step.py --config 3 --warmup 1 --steps 1 > /dev/null 2>&1 && \
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file $OUT/launches_cfg3.csv python tools/profile_step.py --config 3 --warmup 1 --steps 1 > /dev/null 2>&1
+python tools/launch_summary.py $OUT/launches_cfg3.csv > $OUT/launch_summary_cfg3.txt 2>&1
+# full captures of the top kernels
+python tools/gemm_level_probe.py --b 1024 --count 148 > $OUT/gemm_probe.json 2>&1 && \
+  timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_kernel -s 2 -c 1 \
+    -o $OUT/ncu_gemm_level -f python tools/gemm_level_probe.py --b 1024 --count 148 > $OUT/ncu_gemm.log 2>&1
+for spec in "trsm_kernel:40" "lu_panel_kernel:200" "laswp_kernel:40" "dinv_kernel:40"; do
+  name=${spec%%:*}; skip=${spec##*:}
+  timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:"$name" \
+    -s $skip -c 1 -o $OUT/ncu_${name}_cfg3 -f python tools/profile_step.py --config 3 --warmup 1 --steps 1 \
+    > $OUT/ncu_${name}.log 2>&1
+done
+timeout 900 ncu --set full --import-source on --clock-control none --profile-from-start off \
+  -k regex:small_node_kernel -s 2 -c 1 -o $OUT/ncu_small_node_cfg1 -f \
+  python tools/profile_step.py --config 1 --warmup 1 --steps 1 > $OUT/ncu_small.log 2>&1
+python tools/ncu_summary.py $OUT/ncu_*.ncu-rep > $OUT/kernels_ncu.json 2> $OUT/kernels_ncu.err
+echo done
