@@ -730,13 +730,60 @@ class _ArenaExecutor:
 
     def schur(self, items, nids):
         torch = _torch()
-        scratch = [(self.arena.alloc(), self.arena.alloc()) for _ in items]
-        tmp = torch.zeros(len(items), dtype=torch.int32, device=self.device)
-        self.arena.schur([it + sc for it, sc in zip(items, scratch)], tmp)
-        self.st[torch.as_tensor(nids, device=self.device)] = tmp
-        for f, w in scratch:
-            self.arena.release(f)
-            self.arena.release(w)
+        if self.b <= SMALL_MAX or len(items) <= 2:
+            scratch = [(self.arena.alloc(), self.arena.alloc()) for _ in items]
+            tmp = torch.zeros(len(items), dtype=torch.int32, device=self.device)
+            self.arena.schur([it + sc for it, sc in zip(items, scratch)], tmp)
+            self.st[torch.as_tensor(nids, device=self.device)] = tmp
+            for f, w in scratch:
+                self.arena.release(f)
+                self.arena.release(w)
+            self.nodes_run += len(items)
+            return
+        # the rank's nodes of a level share work exactly like a one-GPU level (engine._run_dag):
+        # one factorization per distinct pivot slot, one solve per distinct partner on the
+        # cheaper side, one GEMM-subtract per node (bri_level_batch_ex)
+        ls, rts = {}, {}
+        for p, rt, l_, r, o in items:
+            ls.setdefault(p, set()).add(l_)
+            rts.setdefault(p, set()).add(rt)
+        side = {p: ("rt" if _SOLVE_SIDE != "l" and len(rts[p]) < len(ls[p]) else "l") for p in ls}
+        fidx, sidx, tidx, pos = {}, {}, {}, []
+        fitems, sitems, titems, ritems, gitems, scratch = [], [], [], [], [], []
+        alloc = self.arena.alloc
+        for p, rt, l_, r, o in items:
+            if p not in fidx:
+                f = alloc()
+                fidx[p] = len(fitems)
+                fitems.append((p, f))
+                scratch.append(f)
+            if side[p] == "l":
+                key = ("l", p, l_)
+                if key not in sidx:
+                    w = alloc()
+                    sidx[key] = w
+                    sitems.append((fidx[p], l_, w))
+                    scratch.append(w)
+                gitems.append((rt, sidx[key], r, o))
+            else:
+                if p not in tidx:
+                    ft = alloc()
+                    tidx[p] = len(titems)
+                    titems.append((fidx[p], ft))
+                    scratch.append(ft)
+                key = ("rt", p, rt)
+                if key not in sidx:
+                    s_, c_ = alloc(), alloc()
+                    sidx[key] = c_
+                    ritems.append((tidx[p], rt, s_, c_))
+                    scratch += (s_, c_)
+                gitems.append((sidx[key], l_, r, o))
+            pos.append(fidx[p])
+        tmp = torch.zeros(len(fitems), dtype=torch.int32, device=self.device)
+        self.arena.level(fitems, sitems, gitems, tmp, titems=titems, ritems=ritems)
+        self.st[torch.as_tensor(nids, device=self.device)] = tmp[torch.as_tensor(pos, device=self.device)]
+        for sl in scratch:
+            self.arena.release(sl)
         self.nodes_run += len(items)
 
     def invert(self, h):
@@ -843,7 +890,8 @@ def invert_blocks_sharded(provider: BlockProvider, targets, ws: Workspace | None
     key = (k, tuple(targets)) if (mr is None and mc is None) else None
     sched = _schedule(key, k, specs, None)
     owner = assign_owners(sched, world)
-    need = rank_peak_blocks(sched, owner, rank)
+    # scratch per node: f + w, or (level batch, b > SMALL_MAX) up to f + ft + s + c
+    need = rank_peak_blocks(sched, owner, rank, scratch=4 if src.b > SMALL_MAX else 2)
     budget = _budget_slots(ws, src.b, device)
     # every rank decides the same way (the plans must agree on the transfer sequence)
     import torch
