@@ -145,7 +145,8 @@ cudaError_t launch_rtrsm(const ArenaView& a, const int* gf, int count, const dou
                          cudaStream_t s);
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const CUtensorMap& tmB16,
                               const ArenaView& a, const int* fw, int count, const double* dinv, bool lower, int r0,
-                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s);
+                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s,
+                              const int* didx = nullptr);
 
 // Fused one-CTA node / inverse for n <= SMALL_MAX.
 // items: 5 ints per item (p, rt, l, r, out); mode 0 = Schur node, 1 = inverse of p.

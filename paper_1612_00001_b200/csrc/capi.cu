@@ -550,29 +550,32 @@ int make_dinv(bri_arena* ar, cudaStream_t s, const int* dev_fslots, int count, d
 // columns >= r0 + nr are skipped entirely and the leaves start at each
 // column's diagonal.
 int trsm_rec(bri_arena* ar, cudaStream_t s, const int* fw, const int* gemm_fw, int count, bool lower,
-             int r0, int nr, int nrhs, const double* dinv, bool tri = false, int overlap = 0) {
+             int r0, int nr, int nrhs, const double* dinv, bool tri = false, int overlap = 0,
+             const int* didx = nullptr) {
   const int ncol = tri ? (r0 + nr < nrhs ? r0 + nr : nrhs) : nrhs;
   if (nr <= TRSM_LEAF) {
-    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, ar->v, fw, count, dinv, lower, r0, nr, 0, ncol, tri, s));
+    BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, ar->v, fw, count, dinv, lower, r0, nr, 0, ncol, tri, s,
+                                didx));
     return 0;
   }
   int h = ((nr / 2) + TRSM_BLOCK - 1) / TRSM_BLOCK * TRSM_BLOCK;
   if (h >= nr) h = nr - TRSM_BLOCK;
   if (lower) {
-    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs, dinv, tri, overlap)) return rc;
+    if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, true, r0, h, nrhs, dinv, tri, overlap, didx)) return rc;
     // W[r0+h : r0+nr, :] -= L[r0+h : r0+nr, r0 : r0+h] * W[r0 : r0+h, :]
     const int gcol = tri ? (r0 + h < nrhs ? r0 + h : nrhs) : nrhs;
     if (int rc = gemm_call(ar, s, gemm_fw, count, nr - h, gcol, h, r0 + h, r0, r0, 0, r0 + h, 0, -1.0, 1.0, 0,
                            overlap))
       return rc;
-    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs, dinv, tri, overlap);
+    return trsm_rec(ar, s, fw, gemm_fw, count, true, r0 + h, nr - h, nrhs, dinv, tri, overlap, didx);
   }
-  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs, dinv, false, overlap)) return rc;
+  if (int rc = trsm_rec(ar, s, fw, gemm_fw, count, false, r0 + h, nr - h, nrhs, dinv, false, overlap, didx))
+    return rc;
   // W[r0 : r0+h, :] -= U[r0 : r0+h, r0+h : r0+nr] * W[r0+h : r0+nr, :]
   if (int rc = gemm_call(ar, s, gemm_fw, count, h, nrhs, nr - h, r0, r0 + h, r0 + h, 0, r0, 0, -1.0, 1.0, 0,
                          overlap))
     return rc;
-  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs, dinv, false, overlap);
+  return trsm_rec(ar, s, fw, gemm_fw, count, false, r0, h, nrhs, dinv, false, overlap, didx);
 }
 
 // Both sweeps of dgetrs on W (already row-permuted): L then U.
@@ -1276,6 +1279,8 @@ int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, i
   }
   for (int i = 0; i < nr; ++i) { h.push_back(ritems[4 * i + 2]); h.push_back(ritems[4 * i + 3]); }
   for (int i = 0; i < nr; ++i) h.push_back(titems[2 * ritems[4 * i]]);
+  for (int t = 0; t < nt; ++t) h.push_back(titems[2 * t + 1]);        // Ft slot per transposed factor
+  for (int i = 0; i < nr; ++i) h.push_back(ritems[4 * i]);            // its index, per right solve
   int* dev = nullptr;
   if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
   const int* d_tt = dev + r_base;
@@ -1285,6 +1290,8 @@ int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, i
   const int* d_rfsss = d_rfs + 2 * (size_t)nr;
   const int* d_rsc = d_rfsss + 4 * (size_t)nr;
   const int* d_rfidx = d_rsc + 2 * (size_t)nr;
+  const int* d_tft = d_rfidx + nr;
+  const int* d_rtidx = d_tft + nt;
   const int* d_f = dev;
   const int* d_pf = dev + nf;
   const int* d_ffff = dev + 3 * (size_t)nf;
@@ -1312,7 +1319,12 @@ int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, i
     if (ns > 0) {   // W = U^-1 L^-1 P l with the permutation of the solve's factor
       if (ev_l) BRI_CHECK(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ev_l), cudaEventWaitExternal));
       BRI_CHECK(launch_permcopy(ar->v, d_lw, ns, sc.pi, n, false, st, d_fidx));
-      if (int rc = getrs_sweeps(ar, st, d_fs, d_fw, d_fwww, ns, false, false, 1)) return rc;
+      // diagonal-block inverses once per FACTOR (solves index them through d_fidx); the
+      // factorization already inverted L's diagonal blocks but those of its last outer block
+      double *dl = nullptr, *du = nullptr;
+      if (int rc = make_dinv(ar, st, d_f, nf, &dl, &du, true)) return rc;
+      if (int rc = trsm_rec(ar, st, d_fw, d_fwww, ns, true, 0, n, n, dl, false, 1, d_fidx)) return rc;
+      if (int rc = trsm_rec(ar, st, d_fw, d_fwww, ns, false, 0, n, n, du, false, 1, d_fidx)) return rc;
     }
     if (nr > 0) {   // C = rt^ p^-1 through the transposed factor (the dinv tables reuse the
                     // region the left-side sweeps used: same stream, strictly after them)
@@ -1325,11 +1337,11 @@ int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, i
       transpose_kernel<<<dim3(tb, tb, nr), dim3(32, 8), 0, st>>>(ar->v, d_rs);
       BRI_CHECK(cudaGetLastError());
       double* tl = static_cast<double*>(ar->ctx->dinv.ptr);
-      double* tu = tl + per_dinv * nr;
-      BRI_CHECK(launch_dinv_t(ar->v, d_rft, nr, true, false, tl, 0, 0, st));    // U^T: lower, non-unit
-      BRI_CHECK(launch_dinv_t(ar->v, d_rft, nr, false, true, tu, 0, 0, st));    // L^T: upper, unit
-      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, true, 0, n, n, tl)) return rc;
-      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, false, 0, n, n, tu)) return rc;
+      double* tu = tl + per_dinv * nt;
+      BRI_CHECK(launch_dinv_t(ar->v, d_tft, nt, true, false, tl, 0, 0, st));    // U^T: lower, non-unit
+      BRI_CHECK(launch_dinv_t(ar->v, d_tft, nt, false, true, tu, 0, 0, st));    // L^T: upper, unit
+      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, true, 0, n, n, tl, false, 0, d_rtidx)) return rc;
+      if (int rc = trsm_rec(ar, st, d_rfs, d_rfsss, nr, false, 0, n, n, tu, false, 0, d_rtidx)) return rc;
       count_launch();
       transpose_permute_kernel<<<dim3(tb, tb, nr), dim3(32, 8), 0, st>>>(ar->v, d_rsc, sc.pi, n, d_rfidx);
       BRI_CHECK(cudaGetLastError());

@@ -136,7 +136,8 @@ struct TrsmArgs {
   int ld;
   long long slot_elems;
   const int* items;     // (F, W) per item
-  const double* dinv;   // per item [nblk][T*T]
+  const double* dinv;   // per item [nblk][T*T] (or per factor, through didx)
+  const int* didx;      // optional: item -> index of its dinv table (solves sharing a factor)
   int nblk;
   int r0, nr, c_off, nrhs;
   int tri_rhs;          // LOWER only: right-hand side is unit-lower-triangular (an identity
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(THREADS, 2)
   const int c0 = p.c_off + blockIdx.x * BN;
   const int cend = p.c_off + p.nrhs;
   double* W = p.base + (long long)ws * p.slot_elems;
-  const double* dinv = p.dinv + (long long)item * p.nblk * T * T;
+  const double* dinv = p.dinv + (long long)(p.didx ? p.didx[item] : item) * p.nblk * T * T;
   const int nb = (p.nr + T - 1) / T;
   // both products: 4 warps along M x 2 along N, 16 x BN/2 each; every output
   // element accumulates its k range in ascending k4-steps (splitting k across
@@ -467,13 +468,14 @@ cudaError_t launch_dinv(const ArenaView& a, const int* fslots, int count, bool l
 
 cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, const CUtensorMap& tmB16,
                               const ArenaView& a, const int* fw, int count, const double* dinv, bool lower, int r0,
-                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s) {
+                              int nr, int c_off, int nrhs, bool tri_rhs, cudaStream_t s, const int* didx) {
   TrsmArgs p;
   p.base = a.base;
   p.ld = a.ld;
   p.slot_elems = a.slot_elems;
   p.items = fw;
   p.dinv = dinv;
+  p.didx = didx;
   p.nblk = (a.n + T - 1) / T;
   p.r0 = r0;
   p.nr = nr;
