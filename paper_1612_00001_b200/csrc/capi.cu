@@ -348,13 +348,10 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   // measured on one node + inversion (tools/sweep_caps_large.sh), uncapped vs
   // capped: b = 8192 193.5 -> 166.4 ms, b = 20480 2685 -> 2242 ms; per-block
   // capping once n - J0 <= 4096 (BRI_CAP_ROWS=4096) measured 170 / 2277 ms.
-  // Correctness note: config 5 at b = 20480 (heavy pivoting: off-diagonal
-  // pivot blocks) with BOTH caps forced on (BRI_CAP_ROWS=1000000) returned
-  // wrong, run-dependent blocks in 3 of 3 runs (rel. error 3e-5, 0.34, 0.013);
-  // the trailing cap alone, the fold cap alone and the uncapped default all
-  // give the same bits (3.3e-8 from the Neumann reference).  Capped runs at
-  // n <= 16384 were bit-reproducible (tools/bounded_determinism.py).  Caps
-  // therefore stay restricted to n <= 4096 until that interaction is found.
+  // (Round 1 saw wrong config-5 blocks with both caps forced on; the cause was
+  // the tall-panel pivot race in lu.cu, which long-lived capped GEMMs made
+  // likely — fixed, and with both caps forced config 5 now returns the
+  // uncapped run's exact bits.  The n <= 4096 limit is a speed choice.)
   static const int cap_rows_env = [] {
     const char* e = getenv("BRI_CAP_ROWS");
     return e ? atoi(e) : -1;
