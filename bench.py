@@ -435,8 +435,22 @@ def run_ours(args):
     dom = max(per.items(), key=lambda kv: kv[1])[0] if per else "?"
     dom_fam = FAMILY.get(dom, None)
     shares = {kn: round(us / total_us, 4) for kn, us in sorted(per.items(), key=lambda kv: -kv[1])[:8]}
+    bound, r_unit, r_peak, r_src = "tensor", "TFLOP/s", None, None
     if dom_fam is not None and fam[dom_fam] > 0:
         achieved = fam_flops[dom_fam] / (fam[dom_fam] * 1e-6) / 1e12
+    elif dom == "small_node_kernel" and per.get(dom):
+        # small b (config 1): SURVEY §8(d) asks for HBM GB/s — algorithmic bytes 40 b^2 per node
+        # (4 operand blocks read, 1 written) + 16 b^2 per final inversion, over the kernel's in-step time
+        nodes = len(full_sched.nodes) if not node_shard else len(sched.nodes)
+        algo = (40.0 * nodes + 16.0 * len(cfg["targets"])) * b * b
+        achieved = algo / (per[dom] * 1e-6) / 1e9
+        bound, r_unit = "hbm", "GB/s"
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                r_peak = float(json.load(fh)["hbm_gbs"])
+            r_src = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+        except Exception:
+            r_peak, r_src = 7700.0, "B200 nominal HBM3e (MEASURED_PEAKS.json unreadable)"
     else:
         achieved = None
 
@@ -485,8 +499,9 @@ def run_ours(args):
             "sec_per_block": (ms_all * 1e-3) / max(1, len(my_targets)) if scaling == "weak" else
             (ms_all * 1e-3) / len(cfg["targets"]),
             "fp64_peak_tflops": peak,
-            "roofline": {"bound": "tensor", "kernel": dom, "family": dom_fam, "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+            "roofline": {"bound": bound, "kernel": dom, "family": dom_fam, "achieved": achieved,
+                         "peak": r_peak if bound == "hbm" else peak, "unit": r_unit,
+                         "frac": (achieved / (r_peak if bound == "hbm" else peak)) if achieved else None,
                          "step_share": round(per.get(dom, 0.0) / total_us, 4) if total_us else None,
                          "family_share": round(fam.get(dom_fam, 0.0) / total_us, 4) if dom_fam else None,
                          "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
@@ -495,8 +510,9 @@ def run_ours(args):
                          "method": "one extra untimed step under CUPTI (torch.profiler): family kernel time; "
                                    "executed FLOPs from bri_flop_count over the same step",
                          "isolated": iso,
-                         "peak_source": "bri_fp64_peak DMMA microbenchmark measured in this run "
-                                        "(MEASURED_PEAKS.json has no FP64 figure)"},
+                         "peak_source": r_src if bound == "hbm" else
+                                        ("bri_fp64_peak DMMA microbenchmark measured in this run "
+                                         "(MEASURED_PEAKS.json has no FP64 figure)")},
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_ms},
             "gpu_launches": int(launches),
