@@ -705,29 +705,35 @@ __global__ void pi_snapshot_kernel(const int* pi, int* snap, int n, int nob, int
   for (int x = threadIdx.x; x < n; x += blockDim.x) q[p[x]] = x;
 }
 
-constexpr int LD_WARPS = 4;
-constexpr int LD_MAXN = 4096;   // a warp stages one column segment (< n doubles) in smem
+constexpr int LD_WARPS = 8;
+constexpr int LD_MAXN = 2048;   // orders it handles: 8 column segments (< n doubles) + the composed map fit in smem
 
-// L column c of outer block J (rows >= (J+1)*outer): final[x] = at_J[inv_J[pi[x]]] — the
-// interchanges of every later block at once, one warp per column.
+// All L columns of outer block J (rows >= (J+1)*outer) of one factor, one CTA: the composed map
+// src(x) = inv_J[pi[x]] (where the row now at final position x sat after block J) is built once
+// in smem, then each warp reorders its columns through a staged copy — the interchanges of every
+// later block at once, two coalesced passes per column.
 __global__ void __launch_bounds__(LD_WARPS * 32) laswp_deferred_kernel(ArenaView a, const int* slots,
                                                                        const int* pi, const int* snap,
                                                                        int nob, int outer, int ncols) {
   extern __shared__ double seg_s[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x * LD_WARPS + warp;
-  const int item = blockIdx.y;
-  if (c >= ncols) return;
   const int n = a.n;
-  const int J = c / outer;
+  int* comp = reinterpret_cast<int*>(seg_s + (long long)LD_WARPS * n);   // smem sized by n at launch
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int J = blockIdx.x, item = blockIdx.y;
   const int r0 = (J + 1) * outer;
-  double* col = a.base + (long long)slots[item] * a.slot_elems + (long long)c * a.ld;
   const int* p = pi + (long long)item * n;
   const int* inv = snap + ((long long)item * nob + J) * n;
-  double* seg = seg_s + (long long)warp * LD_MAXN;
-  for (int x = r0 + lane; x < n; x += 32) seg[x - r0] = col[x];
-  __syncwarp();
-  for (int x = r0 + lane; x < n; x += 32) col[x] = seg[inv[p[x]] - r0];
+  for (int x = r0 + threadIdx.x; x < n; x += blockDim.x) comp[x - r0] = inv[p[x]] - r0;
+  __syncthreads();
+  double* seg = seg_s + (long long)warp * n;
+  const int c_end = min((J + 1) * outer, ncols);
+  for (int c = J * outer + warp; c < c_end; c += LD_WARPS) {
+    double* col = a.base + (long long)slots[item] * a.slot_elems + (long long)c * a.ld;
+    for (int x = r0 + lane; x < n; x += 32) seg[x - r0] = col[x];
+    __syncwarp();
+    for (int x = r0 + lane; x < n; x += 32) col[x] = seg[comp[x - r0]];
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------- diag check
@@ -840,7 +846,8 @@ cudaError_t configure_lu() {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_tall_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(laswp_deferred_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, LD_WARPS * LD_MAXN * 8);
+    e = cudaFuncSetAttribute(laswp_deferred_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             LD_WARPS * LD_MAXN * 8 + LD_MAXN * 4);
   return e;
 }
 
@@ -981,8 +988,9 @@ cudaError_t launch_laswp_deferred(const ArenaView& a, const int* slots, int coun
   const int ncols = (nob - 1) * outer;   // the last block has no later interchanges
   if (ncols <= 0) return cudaSuccess;
   count_launch();
-  laswp_deferred_kernel<<<dim3((ncols + LD_WARPS - 1) / LD_WARPS, count), LD_WARPS * 32, LD_WARPS * LD_MAXN * 8,
-                          s>>>(a, slots, pi, snap, nob, outer, ncols);
+  const int smem = LD_WARPS * a.n * 8 + a.n * 4;
+  laswp_deferred_kernel<<<dim3(nob - 1, count), LD_WARPS * 32, smem, s>>>(
+      a, slots, pi, snap, nob, outer, ncols);
   return cudaGetLastError();
 }
 
