@@ -106,6 +106,19 @@ int bri_level_batch_ex(bri_arena* arena, void* stream, int nf, const int* fitems
                        void* ev_l, void* ev_rtr);
 
 /*
+ * A whole small-order DAG run (order <= 96, e.g. BASELINE config 1) in one call and one
+ * CUDA graph — replaces the per-level bri_schur_batch + bri_invert_batch sequence for the
+ * reference's reduce_frame / invert_block recursion (engine.py:196-273) on an HBM-resident M:
+ * gitems (block row, block col, slot) gathered from the row-major device matrix M (leading
+ * dim ldm); nlev levels of lev_counts[l] nodes, nitems 5 ints each (p, rt, l, r, out) in
+ * level order, node_status one int per node; ninv final inversions, iitems (in, out),
+ * inv_status one int each.  Statuses as bri_schur_batch / bri_invert_batch.
+ */
+int bri_dag_small(bri_arena* arena, void* stream, const double* M, long long ldm, int ng, const int* gitems,
+                  int nlev, const int* lev_counts, const int* nitems, int* node_status, int ninv,
+                  const int* iitems, int* inv_status);
+
+/*
  * Block inverses, batched — replaces core.py:238-263 (invert_dense).
  * items: 3 ints per block: slots (in, f, out); f is scratch; in is not modified.
  * status (device, count ints): pivot test of in.

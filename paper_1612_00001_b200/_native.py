@@ -51,6 +51,8 @@ SIGNATURES = [
     ("bri_level_batch", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT, _c_void_p]),
     ("bri_store_host", _c_int, [_c_void_p, _c_void_p, ctypes.c_longlong, _c_void_p, ctypes.c_longlong, _c_int,
                                 _c_int]),
+    ("bri_dag_small", _c_int, [_c_void_p, _c_void_p, _c_void_p, _c_ll, _c_int, _P_INT, _c_int, _P_INT, _P_INT,
+                               _c_void_p, _c_int, _P_INT, _c_void_p]),
     ("bri_level_batch_ex", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT, _c_int,
                                     _P_INT, _c_int, _P_INT, _c_void_p, _c_void_p, _c_void_p]),
     ("bri_level_batch_gated", _c_int, [_c_void_p, _c_void_p, _c_int, _P_INT, _c_int, _P_INT, _c_int, _P_INT,

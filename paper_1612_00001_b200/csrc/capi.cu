@@ -1361,6 +1361,68 @@ int bri_level_batch_ex(bri_arena* ar, void* stream, int nf, const int* fitems, i
   return 0;
 }
 
+// A whole small-order DAG run (b <= SMALL_MAX) as ONE call and one graph: gather the
+// matrix blocks, one one-CTA node launch per level (nodes of a level are independent;
+// level l+1 reads level l's outputs), then the final inversions.  All item arrays go to
+// the device in one upload; per-level launches inside the graph have no host gaps.
+//   gitems: 3 ints (block row, block col, slot), 0-based      -> bri_gather_blocks
+//   nitems: 5 ints (p, rt, l, r, out) per node, levels in order; node_status: one int each
+//   iitems: 2 ints (in, out) per final inversion; inv_status: one int each (ninv may be 0)
+int bri_dag_small(bri_arena* ar, void* stream, const double* M, long long ldm, int ng, const int* gitems,
+                  int nlev, const int* lev_counts, const int* nitems, int* node_status, int ninv,
+                  const int* iitems, int* inv_status) {
+  BRI_NVTX("bri_dag_small");
+  if (ar == nullptr || M == nullptr || ng < 0 || nlev < 0 || ninv < 0 || (ng && !gitems) ||
+      (nlev && (!lev_counts || !nitems || !node_status)) || (ninv && (!iitems || !inv_status)))
+    return fail_msg("bri_dag_small: bad arguments");
+  const int n = ar->v.n;
+  if (n > SMALL_MAX) return fail_msg("bri_dag_small: order > SMALL_MAX uses the level batches");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int nn = 0;
+  for (int l = 0; l < nlev; ++l) {
+    if (lev_counts[l] < 0) return fail_msg("bri_dag_small: negative level count");
+    nn += lev_counts[l];
+  }
+  std::vector<int> h;
+  h.reserve(3 * (size_t)ng + 5 * (size_t)nn + 5 * (size_t)ninv);
+  h.insert(h.end(), gitems, gitems + 3 * (size_t)ng);
+  h.insert(h.end(), nitems, nitems + 5 * (size_t)nn);
+  for (int i = 0; i < ninv; ++i) {   // the node kernel's inverse mode reads (in, -, -, -, out)
+    for (int q = 0; q < 4; ++q) h.push_back(iitems[2 * i]);
+    h.push_back(iitems[2 * i + 1]);
+  }
+  int* dev = nullptr;
+  if (int rc = upload(ar->ctx, s, h, &dev)) return rc;
+  const int* d_g = dev;
+  const int* d_n = dev + 3 * (size_t)ng;
+  const int* d_i = d_n + 5 * (size_t)nn;
+  std::vector<int> counts(lev_counts, lev_counts + nlev);
+  auto issue = [&](cudaStream_t st) -> int {
+    if (ng > 0) {
+      const int gx = n < 1024 ? n : 1024;
+      count_launch();
+      gather_kernel<<<dim3(gx, ng), 256, 0, st>>>(ar->v, M, ldm, d_g);
+      BRI_CHECK(cudaGetLastError());
+    }
+    int off = 0;
+    for (int l = 0; l < nlev; ++l) {
+      BRI_CHECK(launch_small_node(ar->v, d_n + 5 * (size_t)off, counts[l], 0, node_status + off, st));
+      off += counts[l];
+    }
+    if (ninv > 0) BRI_CHECK(launch_small_node(ar->v, d_i, ninv, 1, inv_status, st));
+    return 0;
+  };
+  std::vector<uintptr_t> key = graph_key(5, ar, nn, dev);
+  key.push_back((uintptr_t)M);
+  key.push_back((uintptr_t)ldm);
+  key.push_back((uintptr_t)ng);
+  key.push_back((uintptr_t)ninv);
+  key.push_back((uintptr_t)node_status);
+  key.push_back((uintptr_t)inv_status);
+  for (int l = 0; l < nlev; ++l) key.push_back((uintptr_t)counts[l]);
+  return run_graphed(ar->ctx, s, key, issue);
+}
+
 int bri_gather_blocks(bri_arena* ar, void* stream, const double* M, long long ldm, int count,
                       const int* items) {
   BRI_NVTX("bri_gather_blocks");

@@ -43,8 +43,11 @@ namespace {
 
 // warps per CTA: 8 up to N = 64 (the 64 x 128 augmented block is 32 doubles per lane);
 // 16 for N = 96 so that a lane's share (36 doubles) stays in registers
+#ifndef BRI_SN_WARPS_SMALL
+#define BRI_SN_WARPS_SMALL 8
+#endif
 template <int N>
-constexpr int sn_warps() { return N > 64 ? 16 : 8; }
+constexpr int sn_warps() { return N > 64 ? 16 : BRI_SN_WARPS_SMALL; }
 
 // named barriers (ids 1, 2; 0 is __syncthreads): the producer warp of a step arrives,
 // the others sync — the producer does not wait for its own publication

@@ -101,15 +101,11 @@ class Arena:
         self.handle = handle
         self._free = list(range(nslots - 1, -1, -1))
         self._live = set()
-        self.recorder = None   # list: C-ABI calls of a run are recorded for replay (engine run programs)
-        self.max_live = 0
+        self.max_live = 0      # most slots live at once since the last reset (engine._build_small)
 
     def _call(self, name: str, *args) -> None:
-        """Issue one C-ABI entry point (and record it when a run program is being built)."""
-        fn = getattr(self.lib, name)
-        _native.check(fn(*args), name)
-        if self.recorder is not None:
-            self.recorder.append((fn, args, name))
+        """Issue one C-ABI entry point."""
+        _native.check(getattr(self.lib, name)(*args), name)
 
     # ------------------------------------------------------------ slots
     def alloc(self) -> int:

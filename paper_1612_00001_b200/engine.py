@@ -31,6 +31,7 @@ reduction raises SingularBlockError (core.py:252-254).
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
 import time
@@ -262,25 +263,14 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                    {n: len(v) for n, v in levels.items()}, nslots, chunk)
     # one status tensor (nodes, then roots): one fill, one device -> host read
     nst = max(1, len(sched.nodes))
-    # small orders: the whole run is a handful of C-ABI calls whose arguments depend only on
-    # the schedule, the matrix and the arena — replay the recorded calls (run programs)
-    pkey = None
+    # small orders on an HBM-resident matrix: the whole run is one C-ABI call (bri_dag_small)
+    # whose arrays are built once per (schedule, matrix, arena) and reused
     if trace is None and b <= SMALL_MAX and isinstance(src, _DeviceSource):
-        pkey = (id(sched), b, device, bool(invert_roots), nslots, chunk, src.matrix.data_ptr(),
-                src.matrix.stride(0), threading.get_ident())
-        prog = _PROGRAMS.get(pkey)
-        if prog is not None and prog.sched is sched:
-            arena = cached_arena(b, nslots, device, gauge=ws.gauge)
-            if arena is prog.arena and arena.handle.value == prog.handle:
-                return _replay(prog, arena, sched, ws, info, invert_roots)
-            _PROGRAMS.pop(pkey, None)
+        return _run_dag_small(src, sched, ws, device, invert_roots, info, nslots, chunk, nst)
     st_all = torch.zeros(nst + max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
     status, root_status = st_all[:nst], st_all[nst:]
     results = []
     arena = cached_arena(b, nslots, device, gauge=ws.gauge)
-    out_slots = []
-    if pkey is not None:
-        arena.recorder, arena.max_live = [], 0
     try:
         mslot = {}
         for ij in used:
@@ -407,14 +397,12 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
                     outs.append((f, out))
                 arena.invert(items, root_status[t0:t0 + len(part)])
                 # one gather for the whole chunk (the blocks are views of one result tensor)
-                out_slots.append([out for _, out in outs])
-                results += _gather_slots(arena, out_slots[-1])
+                results += _gather_slots(arena, [out for _, out in outs])
                 for f, out in outs:
                     arena.release(f)
                     arena.release(out)
         else:
-            out_slots.append([val[sched.roots[t]] for t in range(nroots)])
-            results += _gather_slots(arena, out_slots[-1])
+            results += _gather_slots(arena, [val[sched.roots[t]] for t in range(nroots)])
         st_host = st_all.cpu().numpy()  # synchronizes the stream
         node_status = st_host[: len(sched.nodes)]
         rstat = st_host[nst:nst + nroots] if invert_roots else None
@@ -433,60 +421,105 @@ def _run_dag(src, sched, ws: Workspace, device: int, trace=None, invert_roots=Tr
             for t in range(nroots):
                 sched.walk(t, on_node=on_node)
         info.peak_blocks = ws.gauge.peak_blocks
-        if pkey is not None and len(arena.recorder) <= 64:
-            pos_arr = np.zeros(len(sched.nodes), dtype=np.int64)
-            for nid, p_ in pos.items():
-                pos_arr[nid] = p_
-            _PROGRAMS[pkey] = _RunProgram(sched, arena, arena.handle.value, list(arena.recorder), out_slots,
-                                          st_all, pos_arr, nst, arena.max_live, info)
-            if len(_PROGRAMS) > 32:
-                _PROGRAMS.pop(next(iter(_PROGRAMS)))
     finally:
-        arena.recorder = None
         arena.release_all()
     sched.first_failure(pstat, rstat, b)
     return results, info
 
 
 @dataclass
-class _RunProgram:
-    """The C-ABI calls of one small-order DAG run, replayed when the same schedule runs again on the
-    same matrix and arena: no Python item building, no slot bookkeeping (the gauge still sees the
-    run's peak), one status read."""
+class _SmallProgram:
+    """Arrays of one small-order DAG run (bri_dag_small), built once per schedule, matrix and arena:
+    slot of every matrix block / node value / result, node items level by level, the status tensor,
+    and the run's peak live blocks (reported to the gauge on every run)."""
 
     sched: object
     arena: object
     handle: int
-    calls: list           # (fn, args, name); args[1] (the stream) is substituted at replay
-    out_slots: list       # per root chunk: the slots holding the results
-    st_all: object        # the status tensor the recorded calls write into
-    pos_arr: object       # node id -> position of its pivot status
+    args: tuple           # bri_dag_small arguments after (arena, stream)
+    out_slots: list
+    st_all: object
+    pos_arr: object
     nst: int
-    peak: int             # arena blocks live at the run's peak
-    info: RunInfo
+    peak: int
 
 
-_PROGRAMS: "OrderedDict" = OrderedDict()
+_SMALL_PROGRAMS: "OrderedDict" = OrderedDict()
 
 
-def _replay(prog, arena, sched, ws, info, invert_roots):
-    stream = arena.stream
-    for fn, args, name in prog.calls:
-        _native.check(fn(args[0], stream, *args[2:]), name)
+def _build_small(arena, src, sched, invert_roots, nst, device):
+    torch = _torch()
+    levels = sched.levels()
+    used = sorted(sched.m_blocks_used())
+    mslot = {ij: arena.alloc() for ij in used}
+    gitems = [x for (i, j), s_ in mslot.items() for x in (i - 1, j - 1, s_)]
+    val, order, counts, nitems, prev = {}, [], [], [], None
+    slot_of = lambda r: mslot[(r[1], r[2])] if r[0] == "m" else val[r[1]]
+    for n, ids in levels.items():
+        for nid in ids:
+            out = arena.alloc()
+            nitems += [slot_of(r) for r in sched.nodes[nid].operands] + [out]
+            val[nid] = out
+            order.append(nid)
+        counts.append(len(ids))
+        if prev is None:   # the leaves were the only readers of the matrix blocks
+            for s_ in mslot.values():
+                arena.release(s_)
+        else:
+            for nid in prev:
+                arena.release(val.pop(nid))
+        prev = ids
+    iitems, out_slots = [], []
+    if invert_roots:
+        for nid in sched.roots:
+            out = arena.alloc()
+            iitems += [val[nid], out]
+            out_slots.append(out)
+    else:
+        out_slots = [val[nid] for nid in sched.roots]
+    nroots = len(sched.specs)
+    st_all = torch.zeros(nst + max(1, nroots), dtype=torch.int32, device=f"cuda:{device}")
+    pos_arr = np.zeros(len(sched.nodes), dtype=np.int64)
+    for p_, nid in enumerate(order):
+        pos_arr[nid] = p_
+    ia = lambda v: _native.int_array(v) if v else None
+    args = (ctypes.c_void_p(src.matrix.data_ptr()), src.matrix.stride(0), len(used), ia(gitems), len(counts),
+            ia(counts), ia(nitems), ctypes.c_void_p(st_all.data_ptr()), len(iitems) // 2, ia(iitems),
+            ctypes.c_void_p(st_all[nst:].data_ptr()))
+    peak = arena.max_live
+    arena.release_all()
+    return _SmallProgram(sched, arena, arena.handle.value, args, [out_slots], st_all, pos_arr, nst, peak)
+
+
+def _run_dag_small(src, sched, ws, device, invert_roots, info, nslots, chunk, nst):
+    """_run_dag for b <= SMALL_MAX on an HBM-resident matrix: one bri_dag_small call (gather, one
+    one-CTA node launch per level, final inversions: a single CUDA graph); the call's arrays are
+    cached per (schedule, matrix, arena), so a repeated run does no host-side item building."""
+    key = (id(sched), src.b, device, bool(invert_roots), nslots, src.matrix.data_ptr(), src.matrix.stride(0),
+           threading.get_ident())
+    arena = cached_arena(src.b, nslots, device, gauge=None)
+    prog = _SMALL_PROGRAMS.get(key)
+    if prog is None or prog.sched is not sched or prog.arena is not arena or prog.handle != arena.handle.value:
+        arena.max_live = 0
+        prog = _build_small(arena, src, sched, invert_roots, nst, device)
+        _SMALL_PROGRAMS[key] = prog
+        if len(_SMALL_PROGRAMS) > 32:
+            _SMALL_PROGRAMS.popitem(last=False)
+    lib = arena.lib
+    _native.check(lib.bri_dag_small(arena.handle, arena.stream, *prog.args), "bri_dag_small")
+    if ws.gauge is not None and prog.peak:
+        ws.gauge.on_alloc(prog.peak)    # the run held `peak` arena blocks at once
+        ws.gauge.on_release(prog.peak)
     results = []
     for slots in prog.out_slots:
         results += _gather_slots(arena, slots)
     st_host = prog.st_all.cpu().numpy()  # synchronizes the stream
     pstat = st_host[: prog.nst][prog.pos_arr].astype(np.int64)
     rstat = st_host[prog.nst:prog.nst + len(sched.specs)] if invert_roots else None
-    if ws.gauge is not None and prog.peak:
-        ws.gauge.on_alloc(prog.peak)
-        ws.gauge.on_release(prog.peak)
-    run = RunInfo(**{f: getattr(prog.info, f) for f in prog.info.__dataclass_fields__})
-    run.levels = dict(prog.info.levels)
-    run.peak_blocks = ws.gauge.peak_blocks if ws.gauge is not None else prog.peak
-    sched.first_failure(pstat, rstat, arena.n)
-    return results, run
+    info.chunk = max(len(v) for v in sched.levels().values())
+    info.peak_blocks = ws.gauge.peak_blocks if ws.gauge is not None else prog.peak
+    sched.first_failure(pstat, rstat, src.b)
+    return results, info
 
 
 _SOLVE_SIDE = os.environ.get("BRI_SOLVE_SIDE", "auto")   # "auto" | "l" (always W = p^-1 l)

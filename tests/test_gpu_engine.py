@@ -332,9 +332,9 @@ def test_node_sharded_device_executor_world1(bri, golden, monkeypatch):
 
 
 def test_run_program_replay_small_order(bri, golden):
-    """Small-order DAG runs on an HBM-resident matrix replay their recorded C-ABI calls on repeat
-    (engine run programs): the replay returns the same bits, the gauge sees the same peak, the
-    counters advance the same way, and a singular pivot is reported again on replay."""
+    """Small-order DAG runs on an HBM-resident matrix are one bri_dag_small call whose arrays are
+    built once (engine._SMALL_PROGRAMS): a repeat returns the same bits, the gauge sees the same
+    peak, the counters advance the same way, and a singular pivot is reported again."""
     import torch
 
     from paper_1612_00001_b200 import engine
@@ -344,10 +344,10 @@ def test_run_program_replay_small_order(bri, golden):
     targets = [(al, be) for al in range(1, 5) for be in range(1, 5)]
     ws1 = bri.Workspace()
     first, i1 = bri.invert_blocks(prov, targets, ws1)
-    n_prog = len(engine._PROGRAMS)
+    n_prog = len(engine._SMALL_PROGRAMS)
     ws2 = bri.Workspace()
     second, i2 = bri.invert_blocks(prov, targets, ws2)
-    assert len(engine._PROGRAMS) == n_prog and n_prog >= 1
+    assert len(engine._SMALL_PROGRAMS) == n_prog and n_prog >= 1
     for x, y in zip(first, second):
         assert torch.equal(x, y)
     assert ws1.gauge.peak_blocks == ws2.gauge.peak_blocks and ws2.gauge.live_blocks == 0
