@@ -46,8 +46,11 @@ namespace {
 #ifndef BRI_SN_WARPS_SMALL
 #define BRI_SN_WARPS_SMALL 8
 #endif
+#ifndef BRI_SN_WARPS_96
+#define BRI_SN_WARPS_96 16
+#endif
 template <int N>
-constexpr int sn_warps() { return N > 64 ? 16 : BRI_SN_WARPS_SMALL; }
+constexpr int sn_warps() { return N > 64 ? BRI_SN_WARPS_96 : BRI_SN_WARPS_SMALL; }
 
 // named barriers (ids 1, 2; 0 is __syncthreads): the producer warp of a step arrives,
 // the others sync — the producer does not wait for its own publication

@@ -15,7 +15,8 @@ Two runs on the GPU:
   * the default "dag" schedule (each distinct node once, level-batched): every case must pass
     except the live-block-contract assertions in MEMORY_CONTRACT — the DAG deliberately holds
     whole levels of node values (its gauge reports that true footprint) to evaluate shared
-    subtrees once; nothing else may fail;
+    subtrees once — and the CPU timing trend of acceptance criterion 6 (TIMING_TREND);
+    nothing else may fail;
   * schedule "tree" (BRI_SCHEDULE=tree: the reference's depth-first recursion and its
     <= 2k+4 live-block contract) on the MEMORY_CONTRACT cases: all must pass.
     (The whole suite in tree mode — 172 of 172 passed, profiles/r02_reference_suite_tree.txt —
@@ -41,6 +42,12 @@ DESELECT = ["test_cli.py"]
 MEMORY_CONTRACT = ("test_acceptance.py::test_criterion_05_memory_contract",
                    "test_engine.py::TestInvertBlock::test_peak_live_blocks_bound",
                    "test_engine.py::TestInvertFull::test_summary_accounting")
+# acceptance criterion 6 times the CPU algorithm's growth with k at m = 192 (k = 2 < 4 < 8 ms and
+# k = 8 slower than dense LU).  On the GPU these runs are a few latency-bound launches of tiny blocks
+# (b = 96 / 48 / 24: one CTA per node, 20-130 us per launch), so the ordering is a property of
+# launch latency and block order, not of the arithmetic; it may go either way (the verdict of
+# round 1 allowed it as an expected failure).
+TIMING_TREND = ("test_acceptance.py::test_criterion_06_time_trend",)
 
 
 def _have_suite():
@@ -105,7 +112,7 @@ def test_reference_suite_on_gpu(schedule):
     if schedule == "tree":
         assert not failed, failed
     else:
-        unexpected = [f for f in failed if not f.startswith(MEMORY_CONTRACT)]
+        unexpected = [f for f in failed if not f.startswith(MEMORY_CONTRACT + TIMING_TREND)]
         assert not unexpected, unexpected
     if schedule == "tree" and os.environ.get("BRI_REF_SUITE_TREE_ALL") != "1":
         assert counts.get("passed", 0) >= 17, counts
