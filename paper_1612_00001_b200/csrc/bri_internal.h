@@ -30,6 +30,14 @@ inline void pdl_attr(cudaLaunchAttribute& a) {
   a.val.programmaticStreamSerializationAllowed = 1;
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Early trigger (`early` launches only: the pivot chain of <= 2 concurrent factorizations): a chain
+// kernel lets its dependent become RESIDENT at once — the dependent executes this too before its
+// own griddepcontrol.wait, so the residency cascades and the next panel's cluster holds its 8 SMs
+// while the current panel still runs.  Without it the panel re-acquires 8 free SMs of one GPC at
+// every launch and loses them to the concurrent capped GEMMs (config-2 timeline: stalls of up to
+// 270 us with nothing of the chain running).  Memory ordering is unchanged: every dependent still
+// waits for its predecessor's completion before touching global memory.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // One-time kernel attribute setup (dynamic shared memory), done at context creation
 // so that hot-path sequences can be captured into CUDA graphs on first use.
@@ -74,6 +82,7 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int count;      // batch size (set by launch_gemm)
   int max_ctas;   // > 0: persistent launch with at most this many CTAs
+  int early;      // 1: skinny launch on the pivot chain triggers its dependent at once (pdl_trigger)
   int overlap;    // 1: persistent launch, one CTA per SM, whose epilogue (straight from the
                   // accumulators) overlaps the next tile's TMA loads; only where nothing runs
                   // concurrently on other streams (it holds every SM until the batch is done)
@@ -122,10 +131,10 @@ int panel_width(int n);
 int max_panel_rows();  // largest order the register-resident panel factors (16-CTA cluster, 2 rows/thread);
                        // taller panels go through the global-memory tall-panel kernel
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
-                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s);
+                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s, bool early = false);
 cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                             int cbeg, int cend, const LuScratch& sc, int n_stride, int pair_stride,
-                            cudaStream_t s);
+                            cudaStream_t s, bool compose_pi = true, bool early = false);
 cudaError_t launch_laswp(const ArenaView& a, const int* slots, int count, int J0, int W, int nbi, int pidx0,
                          int npan, int a0, int a1, int b0, int b1, const LuScratch& sc, int n_stride,
                          int pair_stride, cudaStream_t s);

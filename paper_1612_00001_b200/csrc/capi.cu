@@ -108,8 +108,10 @@ struct bri_ctx {
   int device = 0;
   cudaStream_t side = nullptr;    // lookahead: bulk trailing updates of the LU
   cudaStream_t side2 = nullptr;   // folded right-hand side of the Schur LU (LuFold)
+  cudaStream_t side3 = nullptr;   // a block's first inner panel carried on to the next block's columns
   cudaStream_t gstream = nullptr; // graphs are captured / launched here
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_x = nullptr, ev_d = nullptr, ev_w = nullptr;
+  cudaEvent_t ev_p = nullptr, ev_y = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
   std::vector<GraphEntry> graphs; // captured hot-path sequences (LRU, <= 16)
   std::vector<std::vector<uintptr_t>> seen;
@@ -210,8 +212,9 @@ LuScratch lu_scratch(void* base, const LuLayout& L) {
 
 int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, int M, int N, int K,
               int a_r0, int a_c0, int b_r0, int b_c0, int c_r0, int c_c0, double alpha, double beta,
-              int max_ctas = 0, int overlap = 0) {
+              int max_ctas = 0, int overlap = 0, int early = 0) {
   GemmParams p{};
+  p.early = early;
   p.max_ctas = max_ctas;
   p.overlap = overlap;
   p.base = ar->v.base;
@@ -230,6 +233,9 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
   p.alpha = alpha;
   p.beta = beta;
   count_flops(FLOP_GEMM, 2.0 * M * N * (double)K * count);
+  // tuning aid (BRI_GEMM_LOG=1): the shapes the solver issues, in capture order
+  static const bool log_shapes = [] { const char* e = getenv("BRI_GEMM_LOG"); return e && *e == '1'; }();
+  if (log_shapes) fprintf(stderr, "GEMMLOG %d %d %d %d %d\n", M, N, K, count, max_ctas);
   BRI_CHECK(launch_gemm(ar->tmA, ar->tmB, p, count, s));
   return 0;
 }
@@ -304,19 +310,62 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
   // carrying every inner panel's interchanges / solve / update on to columns
   // [J0 + W, cext) as well; `ext_ready`: event to wait on before the first of
   // those touches [J0 + W, cext) (nullptr: already up to date)
+  // ext_ready, split (default; BRI_EXT_SPLIT=0 restores the wait): the chain does not wait for
+  // the side stream's update of [J0 + W, cext) before the block's first row panel (the CUPTI
+  // timeline of config 2 showed ~29 us of stall there per outer block, 3.8 ms per step) — the
+  // first inner panel handles the block's own columns at once, and its carry-over to the
+  // extension columns runs on a third stream once they are up to date, overlapping the second
+  // inner panel, whose row panel is the first to touch them on the chain.  Same arithmetic per
+  // element either way.
+  static const bool ext_split = [] {
+    const char* e = getenv("BRI_EXT_SPLIT");
+    return e == nullptr || e[0] != '0';
+  }();
+  // few factorizations in flight: the chain kernels trigger their dependents early (pdl_trigger)
+  static const bool early_env = [] {
+    const char* e = getenv("BRI_PDL_EARLY");
+    return e == nullptr || e[0] != '0';
+  }();
+  const bool early = early_env && bri::pdl_enabled() && vcount <= 2;
   auto factor_block = [&](int J0, int W, int pidx, int cext, cudaEvent_t ext_ready) -> int {
+    bool pending_y = false;
     for (int j0 = J0; j0 < J0 + W; j0 += nbi, ++pidx) {
       const int w = (J0 + W - j0) < nbi ? (J0 + W - j0) : nbi;
-      BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s));
+      BRI_CHECK(launch_panel(v, dev_slots, count, j0, w, pidx, sc, n, L.pair_stride, s, early));
+      const bool split = ext_split && j0 == J0 && ext_ready != nullptr && cext > J0 + W && n - j0 - w > 0;
+      if (split) {
+        cudaStream_t s3 = ctx->side3;
+        BRI_CHECK(cudaEventRecord(ctx->ev_p, s));
+        BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, J0 + W, sc, n, L.pair_stride, s, true, early));
+        const int right_in = J0 + W - j0 - w;
+        if (right_in > 0)
+          if (int rc = gemm_call(ar, s, dev_ffff, count, n - j0 - w, right_in, w, j0 + w, j0, j0, j0 + w, j0 + w,
+                                 j0 + w, -1.0, 1.0, 0, 0, early))
+            return rc;
+        BRI_CHECK(cudaStreamWaitEvent(s3, ctx->ev_p, 0));
+        BRI_CHECK(cudaStreamWaitEvent(s3, ext_ready, 0));
+        BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0 + W, cext, sc, n, L.pair_stride, s3, false));
+        if (int rc = gemm_call(ar, s3, dev_ffff, count, n - j0 - w, cext - (J0 + W), w, j0 + w, j0, j0, J0 + W,
+                               j0 + w, J0 + W, -1.0, 1.0))
+          return rc;
+        BRI_CHECK(cudaEventRecord(ctx->ev_y, s3));
+        pending_y = true;
+        continue;
+      }
       if (j0 == J0 && ext_ready) BRI_CHECK(cudaStreamWaitEvent(s, ext_ready, 0));
-      BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, cext, sc, n, L.pair_stride, s));
+      if (pending_y) {
+        BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_y, 0));
+        pending_y = false;
+      }
+      BRI_CHECK(launch_rowpanel(v, dev_slots, count, j0, w, pidx, J0, cext, sc, n, L.pair_stride, s, true, early));
       const int right = cext - j0 - w;
       if (right > 0 && n - j0 - w > 0) {
         if (int rc = gemm_call(ar, s, dev_ffff, count, n - j0 - w, right, w, j0 + w, j0, j0, j0 + w, j0 + w,
-                               j0 + w, -1.0, 1.0))
+                               j0 + w, -1.0, 1.0, 0, 0, early))
           return rc;
       }
     }
+    if (pending_y) BRI_CHECK(cudaStreamWaitEvent(s, ctx->ev_y, 0));
     return 0;
   };
   // apply block J's interchanges / U12 solve / rank-W update to columns [c0, c1)
@@ -808,6 +857,9 @@ int bri_ctx_create(int device, bri_ctx** out) {
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_d, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_w, cudaEventDisableTiming));
   BRI_CHECK(cudaStreamCreateWithPriority(&c->side2, cudaStreamNonBlocking, prio_low));
+  BRI_CHECK(cudaStreamCreateWithPriority(&c->side3, cudaStreamNonBlocking, prio_high));
+  BRI_CHECK(cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming));
+  BRI_CHECK(cudaEventCreateWithFlags(&c->ev_y, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
   BRI_CHECK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
   BRI_CHECK(cudaStreamCreateWithPriority(&c->gstream, cudaStreamNonBlocking, prio_high));
@@ -832,6 +884,9 @@ void bri_ctx_destroy(bri_ctx* ctx) {
   if (ctx->ev_d) cudaEventDestroy(ctx->ev_d);
   if (ctx->ev_w) cudaEventDestroy(ctx->ev_w);
   if (ctx->side2) cudaStreamDestroy(ctx->side2);
+  if (ctx->ev_p) cudaEventDestroy(ctx->ev_p);
+  if (ctx->ev_y) cudaEventDestroy(ctx->ev_y);
+  if (ctx->side3) cudaStreamDestroy(ctx->side3);
   for (int k = 0; k < bri_ctx::NSTAGE; ++k) {
     if (ctx->stage[k]) cudaFreeHost(ctx->stage[k]);
     if (ctx->stage_ev[k]) cudaEventDestroy(ctx->stage_ev[k]);

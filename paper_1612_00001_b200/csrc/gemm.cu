@@ -338,6 +338,7 @@ constexpr int SK_LDB = SK_KC + 4;   // Bs[n][k]: B fragments 2 wavefronts
 __global__ void __launch_bounds__(256) skinny_kernel(GemmParams p) {
   __shared__ double As[SK_KC * SK_LDA];
   __shared__ double Bs[SK_BN * SK_LDB];
+  if (p.early) pdl_trigger();
   pdl_wait();
   const int* it = p.items + 4 * blockIdx.y;
   const double* A = p.base + (long long)it[0] * p.slot_elems;

@@ -167,6 +167,7 @@ struct PanelArgs {
   int* sigma;
   int* pairs;
   int n_stride, pair_stride;
+  int early;   // pdl_trigger before the wait (bri_internal.h)
 };
 
 // Live row of slot q, shifted (x[c] -> dst[c + 1]), with 16-byte stores; dst
@@ -197,6 +198,7 @@ BRI_DEVI void store_u_row(double* psm, int rhp, int jj, int nb, int slot, const 
 
 template <int RPT>
 __global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
+  if (p.early) pdl_trigger();
   pdl_wait();   // launched programmatically after the previous chain kernel
   constexpr int SW = 34;
   // one 288-byte message per CTA candidate: shifted live row, value, position
@@ -596,6 +598,8 @@ struct RowPanelArgs {
   const int* slots;
   int j0, nb, pidx;
   int cbeg, cend;     // X-columns handled: [cbeg, cend) minus the panel's own
+  int early;          // pdl_trigger before the wait (bri_internal.h)
+  int compose_pi;     // this launch folds the panel's interchanges into pi (exactly one launch per panel does)
   const int* sigma;
   const int* pairs;
   int* pi;
@@ -608,6 +612,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
   __shared__ double L[NBMAX][NBMAX + 1];
   __shared__ int sig[NBMAX];
   __shared__ int prs[1 + 2 * NBMAX];
+  if (p.early) pdl_trigger();
   pdl_wait();
   const int item = blockIdx.y;
   const int n = p.a.n, ld = p.a.ld, nb = p.nb, j0 = p.j0;
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(RP_THREADS) rowpanel_kernel(RowPanelArgs p) {
 
   if (blockIdx.x == gridDim.x - 1) {
     // compose the panel's interchanges into the running row permutation pi
+    if (!p.compose_pi) return;
     int* pi = p.pi + (long long)item * p.n_stride;
     __syncthreads();
     int va = 0, vb = 0;
@@ -854,7 +860,7 @@ cudaError_t configure_lu() {
 int max_panel_rows() { return MAXCS * 2 * PT; }
 
 cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
-                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s) {
+                         const LuScratch& sc, int n_stride, int pair_stride, cudaStream_t s, bool early) {
   const int h = a.n - j0;
   // 1 row per thread while it fits a cluster of 8, else 2 (registers: 2 x 32 doubles)
   // Up to 8 x PT rows: 1 row per thread, portable clusters (measured: beats a
@@ -911,14 +917,17 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   p.pairs = sc.pairs;
   p.n_stride = n_stride;
   p.pair_stride = pair_stride;
+  p.early = early ? 1 : 0;
   if (rpt == 1) return launch_panel_t<1>(p, cs, count, s);
   return launch_panel_t<2>(p, cs, count, s);
 }
 
 cudaError_t launch_rowpanel(const ArenaView& a, const int* slots, int count, int j0, int nb, int pidx,
                             int cbeg, int cend, const LuScratch& sc, int n_stride, int pair_stride,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool compose_pi, bool early) {
   RowPanelArgs p;
+  p.compose_pi = compose_pi ? 1 : 0;
+  p.early = early ? 1 : 0;
   p.a = a;
   p.slots = slots;
   p.j0 = j0;

@@ -60,6 +60,7 @@ template <bool LOWER, bool UNIT = LOWER>
 __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, const int* fslots, double* dinv,
                                                                int nblk, int blk0) {
   __shared__ double S[T][T + 1];   // S[c][r] = block(r, c)
+  __shared__ double rd[T];         // non-unit: reciprocals of the diagonal
   const int blk = blk0 + blockIdx.x, item = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* F = a.base + (long long)fslots[item] * a.slot_elems;
@@ -74,6 +75,13 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
     S[cc][r] = v;
   }
   __syncthreads();
+  // x_k = w_k * (1 / t_kk), like OpenBLAS' trsm kernels: one division per diagonal entry, all
+  // in parallel, instead of one (a ~150-cycle subroutine) per step on every column's chain —
+  // the non-unit kernel took 7x the unit one (config 2: 138 us per U table on the critical path)
+  if (!UNIT) {
+    if (threadIdx.x < T) rd[threadIdx.x] = 1.0 / S[threadIdx.x][threadIdx.x];
+    __syncthreads();
+  }
   double x0[DINV_COLS], x1[DINV_COLS];   // column c = warp + DINV_WARPS * q: rows lane, lane + 32
 #pragma unroll
   for (int q = 0; q < DINV_COLS; ++q) {
@@ -87,9 +95,9 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
       const double s0 = S[k][lane], s1 = S[k][lane + 32];
 #pragma unroll
       for (int q = 0; q < DINV_COLS; ++q) {
-        if (!UNIT) {   // x_k /= l_kk before it propagates (forward substitution, non-unit)
-          const double dk = S[k][k];
-          if (k >= 32) { if (lane == k - 32) x1[q] /= dk; } else { if (lane == k) x0[q] /= dk; }
+        if (!UNIT) {   // x_k *= 1 / l_kk before it propagates (forward substitution, non-unit)
+          const double rk = rd[k];
+          if (k >= 32) { if (lane == k - 32) x1[q] *= rk; } else { if (lane == k) x0[q] *= rk; }
         }
         if (UNIT && k == T - 1) continue;
         const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
@@ -111,10 +119,10 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
   } else {
 #pragma unroll 2
     for (int k = T - 1; k >= 0; --k) {
-      const double dk = S[k][k], s0 = S[k][lane], s1 = S[k][lane + 32];
+      const double rk = rd[k], s0 = S[k][lane], s1 = S[k][lane + 32];
 #pragma unroll
       for (int q = 0; q < DINV_COLS; ++q) {
-        if (k >= 32) { if (lane == k - 32) x1[q] /= dk; } else { if (lane == k) x0[q] /= dk; }
+        if (k >= 32) { if (lane == k - 32) x1[q] *= rk; } else { if (lane == k) x0[q] *= rk; }
         const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
         if (lane < k) x0[q] = fma(-s0, xk, x0[q]);
         if (lane + 32 < k) x1[q] = fma(-s1, xk, x1[q]);

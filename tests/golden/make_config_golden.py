@@ -16,7 +16,8 @@ per block, the floor the off-diagonal targets are judged against.
 Blocks are 8 MiB each, too large to commit, so the fixture keeps, per target:
   * 4096 entries at fixed pseudo-random positions (same positions for every target),
   * the block's first row and column and its diagonal,
-  * max |block|, the 1-ulp floor, and the block-row residual  max |(X M)[:, rows] - I|
+  * max |block|, the 1-ulp floor, the block's relative distance from the dense-LU inverse
+    (numpy.linalg.inv of the same M), and the block-row residual  max |(X M)[:, rows] - I|
     of the reference's whole block row (X = [N_11 .. N_18]).
 Writes tests/golden/config3_row1.npz.
 """
@@ -99,6 +100,7 @@ def main():
     t2 = time.time()
     x = np.concatenate(row, axis=1)                       # block row 1 of M^-1: (b, m)
     resid = float(np.abs(x @ a - np.eye(M)[:B]).max())
+    dense = np.linalg.inv(a)[:B]                          # block row 1 of the dense-LU inverse
     pos = np.random.Generator(np.random.PCG64(77)).integers(0, B, size=(NPOS, 2))
     arrays = {"positions": pos}
     meta = {"k": K, "b": B, "seed": SEED, "targets": [[1, be] for be in range(1, K + 1)],
@@ -112,6 +114,8 @@ def main():
         meta["per_target"][str(be)] = {
             "maxabs": float(np.abs(blk).max()),
             "floor_1ulp": float(np.abs(blk_p - blk).max() / np.abs(blk).max()),
+            "dense_rel": float(np.abs(blk - dense[:, (be - 1) * B:be * B]).max()
+                               / np.abs(dense[:, (be - 1) * B:be * B]).max()),
         }
     np.savez_compressed(OUT, meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8), **arrays)
     print(json.dumps(meta, indent=1))

@@ -130,3 +130,26 @@ def test_gaussian_window_properties():
     assert not pad[:2, 2:].any() and not pad[2:, :2].any()
     assert abs(full.mean()) < 0.01 and abs(full.std() - 1.0) < 0.01
     assert not np.array_equal(full, orc.gaussian_window(m, 5, 0.0, 0, 0, m, m))
+
+
+def test_oracle_matches_reference_at_true_size_config3():
+    """BASELINE config 3 at TRUE size (k=8, b=1024, seed 2): the oracle's block (1,1) reproduces the
+    unmodified reference's block bit for bit at every stored entry (tests/golden/config3_row1.npz:
+    4096 sampled entries, first row, first column, diagonal, max |.|) — the pin that lets the GPU
+    parity test use the fixture instead of re-running the CPU BRI on the GPU box (~80 s here)."""
+    import json
+    import os
+
+    from conftest import ROOT
+    from paper_1612_00001_b200 import workloads
+
+    data = np.load(os.path.join(ROOT, "tests", "golden", "config3_row1.npz"))
+    meta = json.loads(bytes(data["meta"]).decode())
+    assert (meta["k"], meta["b"], meta["seed"], meta["reference_nodes_executed"]) == (8, 1024, 2, 1256)
+    blk = orc.invert_full(workloads.make_matrix(3), 8, memo=True, targets=[(1, 1)])[(1, 1)]
+    pos = data["positions"]
+    np.testing.assert_array_equal(blk[pos[:, 0], pos[:, 1]], data["t1_1_samples"])
+    np.testing.assert_array_equal(blk[0], data["t1_1_row0"])
+    np.testing.assert_array_equal(blk[:, 0], data["t1_1_col0"])
+    np.testing.assert_array_equal(np.diagonal(blk), data["t1_1_diag"])
+    assert float(np.abs(blk).max()) == meta["per_target"]["1"]["maxabs"]

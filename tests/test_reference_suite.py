@@ -18,9 +18,13 @@ Two runs on the GPU:
     subtrees once — and the CPU timing trend of acceptance criterion 6 (TIMING_TREND);
     nothing else may fail;
   * schedule "tree" (BRI_SCHEDULE=tree: the reference's depth-first recursion and its
-    <= 2k+4 live-block contract) on the MEMORY_CONTRACT cases: all must pass.
-    (The whole suite in tree mode — 172 of 172 passed, profiles/r02_reference_suite_tree.txt —
-    takes ~7 minutes; BRI_REF_SUITE_TREE_ALL=1 runs it.)
+    <= 2k+4 live-block contract) on the 18 `test_peak_live_blocks_bound` cases and
+    `test_summary_accounting`: all must pass.  Acceptance criterion 5 asserts the same bound on
+    the same (k, b) grid plus the peak-bytes trend of a k = 8 full inverse repeated three times —
+    a literal tree walk of 1.05 million nodes, ~5 minutes — so it runs in tree mode only with
+    BRI_REF_SUITE_TREE_ALL=1, like the rest of the suite (172 of 172 passed in tree mode,
+    profiles/r02_reference_suite_tree.txt, ~7 minutes): the GPU suite has to fit the driver's
+    20-minute limit.
 
 On CPU only the host-side cases can pass (frames, formats, counters, errors, providers' host
 logic); every computing case must fail loudly with DeviceError — never fall back to the CPU.
@@ -100,7 +104,7 @@ def test_reference_suite_on_gpu(schedule):
         pytest.skip("reference suite not vendored")
     extra = ["-rf"]
     if schedule == "tree" and os.environ.get("BRI_REF_SUITE_TREE_ALL") != "1":
-        extra += ["-k", "memory_contract or peak_live_blocks_bound or summary_accounting"]
+        extra += ["-k", "peak_live_blocks_bound or summary_accounting"]
     rc, counts, text = _run(extra, schedule=schedule)
     report = os.path.join(ROOT, "gpurun_out", f"reference_suite_{schedule}.txt")
     if os.path.isdir(os.path.dirname(report)):
@@ -115,6 +119,6 @@ def test_reference_suite_on_gpu(schedule):
         unexpected = [f for f in failed if not f.startswith(MEMORY_CONTRACT + TIMING_TREND)]
         assert not unexpected, unexpected
     if schedule == "tree" and os.environ.get("BRI_REF_SUITE_TREE_ALL") != "1":
-        assert counts.get("passed", 0) >= 17, counts
+        assert counts.get("passed", 0) >= 19, counts
     else:
         assert counts.get("passed", 0) + len(failed) >= 170, counts
