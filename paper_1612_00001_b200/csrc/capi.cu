@@ -166,6 +166,11 @@ int upload(bri_ctx* ctx, cudaStream_t s, const std::vector<int>& h, int** dev) {
   return 0;
 }
 
+int env_or(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 struct LuLayout {
   int n, count, npanels, pair_stride;
   size_t off_ipiv, off_pi, off_sigma, off_pairs, off_scale, off_status, off_orig, off_snap, total;
@@ -406,7 +411,33 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     return e ? atoi(e) : -1;
   }();
   const int cap_rows = cap_rows_env >= 0 ? cap_rows_env : (n > 4096 ? 0 : 0x7fffffff);
-  auto capped = [&](int J0, int cap) { return (n - J0) <= cap_rows ? cap : 0; };
+  // Default caps follow the work: the trailing update of block J shrinks like (n - J0)^2, the
+  // fold like (n - J0) * n, and the fold has no deadline but the end of the factorization, so it
+  // gets the SMs the trailing update (which the chain waits for, one block behind) no longer
+  // needs to finish inside one block of the chain (~190 us at ~0.16 TFLOP/s per CTA on K = 128
+  // tiles): trail(J) = 132 r^2 clamped to [24, 80], fold(J) = 124 - trail(J + 2) — the fold runs
+  // about two blocks behind the chain — with r = (n - J0) / n; the chain keeps 16 SMs for its two
+  // resident panel clusters.  With the fixed 80 / 48 pair the fold trailed the chain by ~8 blocks
+  // on config 2 and finished 1.3 ms after it on 48 SMs (CUPTI timeline); giving the trailing
+  // update 100 CTAs early on starved the fold instead (24 CTAs: 1 ms per block).
+  // BRI_DYN_CAPS=0 or an explicit BRI_TRAIL_CAP / BRI_FOLD_CAP keeps fixed caps.
+  static const bool dyn_caps_env = [] {
+    const char* e = getenv("BRI_DYN_CAPS");
+    return e == nullptr || e[0] != '0';
+  }();
+  const bool dyn_caps = dyn_caps_env && trail_cap_env < 0 && fold_cap_env < 0 && vcount <= 2;
+  auto capped = [&](int J0, int cap, bool trailing) {
+    if ((n - J0) > cap_rows || cap <= 0) return 0;
+    if (!dyn_caps) return cap;
+    static const int cap_a = env_or("BRI_CAP_A", 132), cap_hi = env_or("BRI_CAP_HI", 80),
+                     cap_lag = env_or("BRI_CAP_LAG", 2);
+    auto trail_at = [&](int j0) {
+      const double r = j0 < n ? (double)(n - j0) / n : 0.0;
+      const int t = (int)(cap_a * r * r + 0.5);
+      return t < 24 ? 24 : (t > cap_hi ? cap_hi : t);
+    };
+    return trailing ? trail_at(J0) : 124 - trail_at(J0 + cap_lag * outer);
+  };
   // W <- L11^-1 P_J W on block J's rows, then W[N0:, :] -= L21 W[J rows, :]
   auto fold_block = [&](cudaStream_t st, int J0, int W, int pidx0, int npan) -> int {
     const bool tri = fold->tri;
@@ -424,7 +455,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(launch_trsm_fused(ar->tmA, ar->tmB32, ar->tmB16, v, fold->fw, count, dl, true, J0, W, 0, ncol, tri, st));
     if (n - J0 - W > 0)
       return gemm_call(ar, st, fold->fwww, count, n - J0 - W, ncol, W, J0 + W, J0, J0, 0, J0 + W, 0, -1.0, 1.0,
-                       capped(J0, fold_cap));
+                       capped(J0, fold_cap, false));
     return 0;
   };
   double* du = dl + per * count;
@@ -438,7 +469,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
     BRI_CHECK(launch_rtrsm(v, fold->gf, count, du, J0, W, st));
     if (n - J0 - W > 0)
       return gemm_call(ar, st, fold->gfgg, count, n, n - J0 - W, W, 0, J0, J0, J0 + W, 0, J0 + W, -1.0, 1.0,
-                       capped(J0, fold_cap));
+                       capped(J0, fold_cap, false));
     return 0;
   };
   // C part of block J once its U row block is final (recorded as ev_b on s1)
@@ -517,7 +548,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       BRI_CHECK(cudaStreamWaitEvent(s1, ctx->ev_a, 0));
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N1, n, capped(J0, trail_cap))) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N1, n, capped(J0, trail_cap, true))) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1, nullptr)) return rc;
@@ -536,7 +567,7 @@ int getrf_device(bri_arena* ar, cudaStream_t s, const int* dev_slots, const int*
       }
       BRI_CHECK(launch_laswp(v, dev_slots, count, J0, W, nbi, pidx0, npan, 0, J0 * left, N1 + WNN, n, sc, n,
                              L.pair_stride, s1));
-      if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, capped(J0, trail_cap))) return rc;
+      if (int rc = update_cols(s1, J0, W, pidx0, N1 + WNN, n, capped(J0, trail_cap, true))) return rc;
       BRI_CHECK(cudaEventRecord(ctx->ev_b, s1));
       if (int rc = fold_c_after_b(J0, W)) return rc;
       if (int rc = factor_block(N0, WN, pidx0 + npan_outer, N1 + WNN, WNN > 0 ? ctx->ev_x : nullptr)) return rc;
