@@ -1,5 +1,5 @@
 for rep in 1 2; do
-for cfg in "132 80 2" "160 88 2" "160 96 3" "150 80 2" "132 80 3" "180 100 4"; do
-set -- $cfg
-BRI_CAP_A=$1 BRI_CAP_HI=$2 BRI_CAP_LAG=$3 timeout 300 python bench.py --config 2 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/s5_cap_$1_$2_$3_r$rep.log 2>&1
+for e in 1 0; do
+BRI_PDL_EARLY=$e BRI_EXT_SPLIT=$e timeout 600 python bench.py --config 2 --b 8192 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s5_b8192_e${e}_r$rep.log 2>&1
+BRI_PDL_EARLY=$e BRI_EXT_SPLIT=$e timeout 600 python bench.py --config 2 --b 2048 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/s5_b2048_e${e}_r$rep.log 2>&1
 done; done

@@ -485,7 +485,11 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
   if (p.max_ctas > 0 && ctas > p.max_ctas) ctas = p.max_ctas;
   if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
   count_launch();
+  // capped launches of short-K updates (the LU's rank-128 trailing and fold GEMMs next to the
+  // pivot chain): a CTA's next tile starts loading during its epilogue (BRI_CAP_OVERLAP)
+  static const int cap_overlap = env_int("BRI_CAP_OVERLAP", 0);
   if (ctas < (long long)p.tiles_m * p.tiles_n * count) {
+    p.overlap = (cap_overlap && p.K <= cap_overlap) ? 1 : 0;
     gemm_persistent_kernel<<<dim3((unsigned)ctas), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
   } else {
     gemm_kernel<<<dim3(p.tiles_m * p.tiles_n, count), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
