@@ -1,5 +1,5 @@
+BRI_TRSM_BN64=2 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py -q -p no:cacheprovider -x -rf > gpurun_out/s5_bn64_tests.log 2>&1; echo rc=$? >> gpurun_out/s5_bn64_tests.log
 for rep in 1 2; do
-for e in 1 0; do
-BRI_PDL_EARLY=$e BRI_EXT_SPLIT=$e timeout 600 python bench.py --config 2 --b 8192 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/s5_b8192_e${e}_r$rep.log 2>&1
-BRI_PDL_EARLY=$e BRI_EXT_SPLIT=$e timeout 600 python bench.py --config 2 --b 2048 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/s5_b2048_e${e}_r$rep.log 2>&1
+for w in 1 0; do
+BRI_TRSM_BN64=$w timeout 600 python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/s5_bn64_${w}_r$rep.log 2>&1
 done; done

@@ -27,7 +27,9 @@ struct StageGeom {
 };
 
 // Issue the TMA loads of one k-tile into stage buffer `st` (called by one lane).
-template <int BM, int BN>
+// NBOX: the B operand arrives as NBOX boxes of BN / NBOX columns each through a narrower map (the
+// [n][k] rows are 128 bytes, so consecutive boxes form the same swizzled layout as one wide box).
+template <int BM, int BN, int NBOX = 1>
 BRI_DEVI void tile_issue(uint8_t* st, uint64_t* full, const CUtensorMap* tmA, const CUtensorMap* tmB,
                          int a_row, int a_col, int a_slot, int b_row, int b_col, int b_slot) {
   mbar_arrive_expect_tx(full, StageGeom<BM, BN>::BYTES);
@@ -38,7 +40,10 @@ BRI_DEVI void tile_issue(uint8_t* st, uint64_t* full, const CUtensorMap* tmA, co
 #pragma unroll
   for (int ob = 0; ob < BM / 8; ++ob) tma_load_3d(st + ob * 1024, tmA, full, a_row + ob * 8, a_col, a_slot);
 #endif
-  tma_load_3d(st + StageGeom<BM, BN>::A_BYTES, tmB, full, b_row, b_col, b_slot);
+#pragma unroll
+  for (int h = 0; h < NBOX; ++h)
+    tma_load_3d(st + StageGeom<BM, BN>::A_BYTES + h * (StageGeom<BM, BN>::B_BYTES / NBOX), tmB, full, b_row,
+                b_col + h * (BN / NBOX), b_slot);
 }
 
 // Warp-level accumulator of a (16*MI) x (8*NJ) sub-tile.

@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
   constexpr int SB = StageGeom<T, BN>::BYTES;
   constexpr int XJ = BN / 16;       // n8 tiles per warp (4 warps along M x 2 along N, 16 x BN/2 each)
+  constexpr int NBOX = BN > 32 ? BN / 32 : 1;   // BN = 64 loads its X tiles as two 32-column boxes (tmB32)
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (TMA 128B swizzle atoms) by pointer arithmetic on the
   // __shared__ array, so the compiler keeps the shared address space (LDS, not
@@ -210,8 +211,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int KT = K > 0 ? (K + TILE_BK - 1) / TILE_BK : 0;
     auto issue = [&](int kt) {
       const int s = (it + kt) % STAGES;
-      tile_issue<T, BN>(smem + s * SB, &full[s], &tmA, &tmB, row0, klo + kt * TILE_BK, fs,
-                        klo + kt * TILE_BK, c0, ws);
+      tile_issue<T, BN, NBOX>(smem + s * SB, &full[s], &tmA, &tmB, row0, klo + kt * TILE_BK, fs,
+                              klo + kt * TILE_BK, c0, ws);
     };
     if (producer)
       for (int kt = pre; kt < STAGES && kt < KT; ++kt) issue(kt);
@@ -263,8 +264,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int kt = 0; kt < safe; ++kt) {
         const int q = it + kt;
         if (q >= STAGES) mbar_wait(&empty[q % STAGES], ((q / STAGES) - 1) & 1);
-        tile_issue<T, BN>(smem + (q % STAGES) * SB, &full[q % STAGES], &tmA, &tmB, row0n,
-                          klo + kt * TILE_BK, fs, klo + kt * TILE_BK, c0, ws);
+        tile_issue<T, BN, NBOX>(smem + (q % STAGES) * SB, &full[q % STAGES], &tmA, &tmB, row0n,
+                                klo + kt * TILE_BK, fs, klo + kt * TILE_BK, c0, ws);
       }
       pre = safe;
     }
@@ -424,6 +425,8 @@ cudaError_t configure_trsm() {
   };
   set((const void*)trsm_kernel<true, 32, 3>, smem_bytes<32, 3>());
   set((const void*)trsm_kernel<false, 32, 3>, smem_bytes<32, 3>());
+  set((const void*)trsm_kernel<true, 64, 4>, smem_bytes<64, 4>());
+  set((const void*)trsm_kernel<false, 64, 4>, smem_bytes<64, 4>());
   set((const void*)trsm_kernel<true, 16, 4>, smem_bytes<16, 4>());
   set((const void*)trsm_kernel<false, 16, 4>, smem_bytes<16, 4>());
   set((const void*)rtrsm_kernel, RT_SMEM);
@@ -496,7 +499,12 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return v;
   }();
-  const bool fine = (long long)((nrhs + 31) / 32) * count <= sms;
+  bool fine = (long long)((nrhs + 31) / 32) * count <= sms;
+  // BRI_TRSM_BN64: 1 = large batches (at least two CTAs of 64 columns per SM), 2 = always (tests)
+  static const int wide_env = [] {
+    const char* e = getenv("BRI_TRSM_BN64");
+    return e != nullptr ? atoi(e) : 0;
+  }();
   // nr x nr triangle against nrhs columns (tri_rhs: column c starts at its diagonal)
   double per = (double)nr * nr * nrhs;
   if (tri_rhs) {
@@ -510,10 +518,18 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
   }
   count_flops(FLOP_TRSM, per * count);
   count_launch();
+  if (wide_env >= 2 && nrhs >= 64) fine = false;
   if (fine) {
     dim3 grid((nrhs + 15) / 16, count);
     if (lower) trsm_kernel<true, 16, 4><<<grid, THREADS, smem_bytes<16, 4>(), s>>>(tmA, tmB16, p);
     else trsm_kernel<false, 16, 4><<<grid, THREADS, smem_bytes<16, 4>(), s>>>(tmA, tmB16, p);
+  } else if (wide_env && nrhs >= 64 && (wide_env >= 2 || (long long)((nrhs + 63) / 64) * count >= 2 * sms)) {
+    // large batches: 64 columns per CTA (one CTA per SM) — half the T-tile traffic per flop and
+    // 16 x 32 warp tiles (1.5 instead of 2 fragment loads per DMMA: ncu shows the 32-column
+    // kernel at 73% of the shared-memory pipe with the DMMA pipe at 58-69%)
+    dim3 grid((nrhs + 63) / 64, count);
+    if (lower) trsm_kernel<true, 64, 4><<<grid, THREADS, smem_bytes<64, 4>(), s>>>(tmA, tmB32, p);
+    else trsm_kernel<false, 64, 4><<<grid, THREADS, smem_bytes<64, 4>(), s>>>(tmA, tmB32, p);
   } else {
     dim3 grid((nrhs + 31) / 32, count);
     if (lower) trsm_kernel<true, 32, 3><<<grid, THREADS, smem_bytes<32, 3>(), s>>>(tmA, tmB32, p);

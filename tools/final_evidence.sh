@@ -5,12 +5,14 @@
 set -u
 OUT=gpurun_out/final
 mkdir -p $OUT
-python -m pytest tests -m gpu -q -p no:cacheprovider -rf > $OUT/gputest.log 2>&1; echo "rc=$?" >> $OUT/gputest.log
-python bench.py > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err; echo "rc=$?" >> $OUT/bench_cfg3.err
-python bench.py --impl reference > $OUT/ref_cfg3.json 2> $OUT/ref_cfg3.err
-python bench.py --config 1 > $OUT/bench_cfg1.json 2> $OUT/bench_cfg1.err
-python bench.py --config 2 > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err
-python tools/timeline.py --config 3 --out $OUT/timeline_cfg3.json > $OUT/timeline_cfg3.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=12 > $OUT/gputest.log 2>&1; echo "rc=$?" >> $OUT/gputest.log
+timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err; echo "rc=$?" >> $OUT/bench_cfg3.err
+( time timeout 1500 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/ref_cfg3.json ) 2> $OUT/ref_cfg3.err
+timeout 600 python bench.py --config 1 --steps 20 --warmup 5 > $OUT/bench_cfg1.json 2> $OUT/bench_cfg1.err
+timeout 600 python bench.py --config 2 --steps 20 --warmup 5 > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err
+timeout 600 python tools/timeline.py --config 3 --out $OUT/timeline_cfg3.json > $OUT/timeline_cfg3.txt 2>&1
+timeout 600 python tools/timeline.py --config 2 --out $OUT/timeline_cfg2.json > $OUT/timeline_cfg2.txt 2>&1
+python tools/chain_gaps.py $OUT/timeline_cfg2.json > $OUT/chain_cfg2.txt 2>&1
 # launch list: one config-3 step (cold-cache, serialised: compare shares, not absolutes)
 python tools/profile_step.py --config 3 --warmup 1 --steps 1 > /dev/null 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
@@ -30,4 +32,6 @@ timeout 900 ncu --set full --import-source on --clock-control none --profile-fro
   -k regex:small_node_kernel -s 2 -c 1 -o $OUT/ncu_small_node_cfg1 -f \
   python tools/profile_step.py --config 1 --warmup 1 --steps 1 > $OUT/ncu_small.log 2>&1
 python tools/ncu_summary.py $OUT/ncu_*.ncu-rep > $OUT/kernels_ncu.json 2> $OUT/kernels_ncu.err
+# config 5 at true size with the final build (bounded schedule, ~7 min), Neumann check and hash
+timeout 1500 python tools/run_config5.py --terms 2 --out $OUT/config5.json > $OUT/config5.log 2>&1
 echo done
