@@ -88,13 +88,27 @@ __device__ unsigned long long g_small_phase[8];
 #endif
 
 // mode 0: Schur node (items: p, rt, l, r, out);  mode 1: out = p^-1 (items: in, -, -, -, out)
-template <int N>
+//
+// BLK (opt-in, BRI_SMALL_BLOCKED=1): the columns are dealt to the warps in BLOCKS (warp w owns matrix and right-hand-
+// side columns [w * QM, (w + 1) * QM)), and a warp factors its whole QM-column panel by itself —
+// pivot search, multipliers and the panel's own rank-1 updates all inside one warp, no CTA barrier
+// and no shared-memory round trip per column — then publishes the panel's QM multiplier columns
+// once (one named barrier per PANEL instead of per column).  The other warps apply the panel to
+// their columns step by step (same fma(-l_ij, u_jc, a_ic), same j order: results are bit-identical
+// to the column-cyclic schedule); the owner of the next panel updates its matrix columns first,
+// factors and publishes, and only then catches up on its right-hand-side columns, so the critical
+// path is the chain of panel factorizations.  Measured (tools/bench_small.sh): bit-identical outputs
+// and the same time per launch as the default column-cyclic schedule (!BLK: one barrier per column,
+// owner of column j + 1 looks ahead) — 60.0 vs 60.2 us at N = 64 — so the per-column cost is not
+// the barrier protocol but the dependent chain of a pivot step itself.
+template <int N, bool BLK>
 __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(ArenaView a, const int* items, int mode,
                                                                          int* status) {
   constexpr int NW = sn_warps<N>();
   constexpr int SN_THREADS = 32 * NW;
   constexpr int R = N / 32;        // rows per lane
   constexpr int Q = 2 * N / NW;    // augmented columns per warp (N of p^, N of the right-hand side)
+  constexpr int QM = Q / 2;        // matrix columns per warp
   constexpr int LDR = sn_ldr<N>();
   extern __shared__ double sm[];
   double* RTs = sm;                // RTs[k * LDR + i] = rt^(i, k)
@@ -113,6 +127,10 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   const double* Rb = a.base + (long long)it[3] * a.slot_elems;
   double* Out = a.base + (long long)it[4] * a.slot_elems;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // augmented column held in register column q: matrix columns are < N, right-hand side N + c
+  auto colof = [&](int q) {
+    return BLK ? (q < QM ? warp * QM + q : N + warp * QM + (q - QM)) : warp + NW * q;
+  };
 #ifdef BRI_SMALL_PROFILE
   unsigned long long t_last = clock64();
 #endif
@@ -143,7 +161,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     pos[h] = r;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-      const int c = warp + NW * q;
+      const int c = colof(q);
       double v = 0.0;
       if (c < N) {
         if (r < n && c < n) v = P[r + (long long)c * ld];
@@ -225,6 +243,124 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   };
   // make the max |p| reduction and the zeroed smem visible before the sweep
   __syncthreads();
+  if constexpr (BLK) {
+    __shared__ double bmult[3][QM][N];   // a panel's multiplier columns, by physical row (3 panels in flight)
+    __shared__ int prow_b[N], ppos_b[N];
+    // Factor this warp's panel pw (register columns 0 .. QM-1, steps j = pw * QM + jq): dgetf2
+    // inside one warp.  Per step: argmax |x| over the rows at positions >= j (ties -> smallest
+    // position, NaN never wins), multipliers x * (1/pivot) kept in place and published, the
+    // position bookkeeping of the interchange, and the rank-1 update of the panel's own columns
+    // right of j.
+    auto factor_panel = [&](int pw) {
+      double(*bm)[N] = bmult[pw % 3];
+#pragma unroll
+      for (int jq = 0; jq < QM; ++jq) {
+        const int j = pw * QM + jq;
+        if (j >= n) break;
+        double bv = -1.0;
+        int bi = INT_MAX;
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          const int r = lane + 32 * h;
+          const double av = fabs(A[h][jq]);
+          if (r < n && pos[h] >= j && (av > bv || (av == bv && pos[h] < bi))) {
+            bv = av;
+            bi = pos[h];
+          }
+        }
+        warp_argmax_fast(bv, bi);
+        const int pp = (bi == INT_MAX) ? j : bi;   // all NaN: pivot in place
+        int oh = -1;
+#pragma unroll
+        for (int h = 0; h < R; ++h)
+          if (lane + 32 * h < n && pos[h] == pp) oh = h;
+        double mine = 0.0;
+#pragma unroll
+        for (int h = 0; h < R; ++h)
+          if (oh == h) mine = A[h][jq];
+        const unsigned m = __ballot_sync(0xffffffffu, oh >= 0);
+        const int src = __ffs(m) - 1;
+        const double pv = __shfl_sync(0xffffffffu, mine, src);
+        const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
+        const bool recip = fabs(pv) >= kSfmin;
+        const double rinv = 1.0 / pv;
+        double lm[R];
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          const int r = lane + 32 * h;
+          double l = 0.0;
+          if (r < n && pos[h] >= j && r != rp && pv != 0.0) {
+            l = recip ? A[h][jq] * rinv : A[h][jq] / pv;
+            A[h][jq] = l;
+          }
+          lm[h] = l;
+          bm[jq][r] = l;
+        }
+        if (lane == 0) {
+          prow_b[j] = rp;
+          ppos_b[j] = pp;
+          pvs[j] = pv;
+        }
+#pragma unroll
+        for (int h = 0; h < R; ++h) {
+          if (pos[h] == j) pos[h] = pp;           // the row at position j takes the pivot's place
+          else if (lane + 32 * h == rp) pos[h] = j;
+        }
+        const int srcl = rp & 31, hp = rp >> 5;
+#pragma unroll
+        for (int q = jq + 1; q < QM; ++q) update_col(q, lm, srcl, hp);
+      }
+    };
+    // Apply the published panel pw to this warp's columns, one pivot step at a time.
+    auto apply_panel = [&](int pw, bool do_pos, bool do_mat, bool do_rhs) {
+      double(*bm)[N] = bmult[pw % 3];
+#pragma unroll
+      for (int jq = 0; jq < QM; ++jq) {
+        const int j = pw * QM + jq;
+        if (j >= n) break;
+        const int rp = prow_b[j], pp = ppos_b[j];
+        const int srcl = rp & 31, hp = rp >> 5;
+        double lm[R];
+#pragma unroll
+        for (int h = 0; h < R; ++h) lm[h] = bm[jq][lane + 32 * h];
+        if (do_pos) {
+#pragma unroll
+          for (int h = 0; h < R; ++h) {
+            if (pos[h] == j) pos[h] = pp;
+            else if (lane + 32 * h == rp) pos[h] = j;
+          }
+        }
+        if (do_mat) {
+#pragma unroll
+          for (int q = 0; q < QM; ++q) update_col(q, lm, srcl, hp);
+        }
+        if (do_rhs) {
+#pragma unroll
+          for (int q = QM; q < Q; ++q) update_col(q, lm, srcl, hp);
+        }
+      }
+    };
+    if (warp == 0 && n > 0) {
+      factor_panel(0);
+      __syncwarp();
+      bar_arrive(1, SN_THREADS);
+    }
+#pragma unroll 1
+    for (int pw = 0; pw < NW; ++pw) {
+      if (pw * QM >= n) break;
+      const bool owner = (warp == pw);
+      if (!owner) bar_sync(1 + (pw & 1), SN_THREADS);   // panel pw is published
+      if (warp == pw + 1 && (pw + 1) * QM < n) {
+        apply_panel(pw, true, true, false);
+        factor_panel(pw + 1);
+        __syncwarp();
+        bar_arrive(1 + ((pw + 1) & 1), SN_THREADS);
+        apply_panel(pw, false, false, true);
+      } else {
+        apply_panel(pw, !owner, warp > pw, true);
+      }
+    }
+  } else {
   if (warp == 0 && n > 0) {
     pivot_step(0, 0);
     bar_arrive(1, SN_THREADS);
@@ -280,6 +416,8 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     }
   }
 
+  }   // !BLK
+
   SPROF(1);
   // ------------------------------------------------ backward sweep (dgetrs' U solve), no barriers
   //   x_k = w_k * (1/u_kk);  w_i -= u_ik x_k  (i < k),  k descending.  U is static by now:
@@ -287,6 +425,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   //   and every warp then solves its own right-hand-side columns independently.
   {
     __shared__ int row_at[N];
+    __shared__ double rpv[N];   // 1 / u_kk, one division per pivot in parallel (was one per step on every warp's chain)
     double* Us = Ws;   // U(r, k) at Us[k * LDR + r] (physical row r); Ws is rebuilt afterwards
     __syncthreads();
 #pragma unroll
@@ -295,15 +434,16 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       if (warp == 0 && r < n) row_at[pos[h]] = r;
 #pragma unroll
       for (int q = 0; q < Q / 2; ++q) {      // matrix columns of this warp
-        const int c = warp + NW * q;
+        const int c = colof(q);
         if (c < n && r < N) Us[c * LDR + r] = (r < n && pos[h] < c) ? A[h][q] : 0.0;
       }
     }
+    for (int k = tid; k < n; k += SN_THREADS) rpv[k] = 1.0 / pvs[k];
     __syncthreads();
     for (int k = n - 1; k >= 0; --k) {
       const int rk = row_at[k];
       const int srcl = rk & 31, hk = rk >> 5;
-      const double rkk = 1.0 / pvs[k];
+      const double rkk = rpv[k];
       double um[R];
 #pragma unroll
       for (int h = 0; h < R; ++h) um[h] = Us[k * LDR + lane + 32 * h];
@@ -336,7 +476,7 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
       const int k = pos[h];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const int c = warp + NW * q - N;
+        const int c = colof(q) - N;
         if (c >= 0 && c < n) {
           const double x = A[h][q];
           if (mode == 1) Out[k + (long long)c * ld] = x;
@@ -380,11 +520,24 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
   SPROF(5);
 }
 
+int g_small_blocked = -1;   // -1: BRI_SMALL_BLOCKED (default 0: measured equal at N = 32 / 64, 4% slower at N = 96)
+
+bool small_blocked() {
+  if (g_small_blocked < 0) {
+    const char* e = getenv("BRI_SMALL_BLOCKED");
+    g_small_blocked = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return g_small_blocked != 0;
+}
+
 template <int N>
 cudaError_t launch_small_t(const ArenaView& a, const int* items, int count, int mode, int* status,
                            cudaStream_t s) {
   count_launch();
-  small_node_kernel<N><<<count, 32 * sn_warps<N>(), small_smem<N>(), s>>>(a, items, mode, status);
+  if (small_blocked())
+    small_node_kernel<N, true><<<count, 32 * sn_warps<N>(), small_smem<N>(), s>>>(a, items, mode, status);
+  else
+    small_node_kernel<N, false><<<count, 32 * sn_warps<N>(), small_smem<N>(), s>>>(a, items, mode, status);
   return cudaGetLastError();
 }
 
@@ -398,14 +551,19 @@ void small_profile_read(unsigned long long* out) {
 }
 #endif
 
+void small_set_blocked(int on) { g_small_blocked = on ? 1 : 0; }   // tools: switch schedules in one process
+
 cudaError_t configure_small() {
-  cudaError_t e = cudaFuncSetAttribute(small_node_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       small_smem<32>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(small_node_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, small_smem<64>());
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(small_node_kernel<SMALL_MAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             small_smem<SMALL_MAX>());
+  cudaError_t e = cudaSuccess;
+  auto set = [&](const void* f, int bytes) {
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  };
+  set((const void*)small_node_kernel<32, true>, small_smem<32>());
+  set((const void*)small_node_kernel<32, false>, small_smem<32>());
+  set((const void*)small_node_kernel<64, true>, small_smem<64>());
+  set((const void*)small_node_kernel<64, false>, small_smem<64>());
+  set((const void*)small_node_kernel<SMALL_MAX, true>, small_smem<SMALL_MAX>());
+  set((const void*)small_node_kernel<SMALL_MAX, false>, small_smem<SMALL_MAX>());
   return e;
 }
 

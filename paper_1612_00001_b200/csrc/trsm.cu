@@ -75,13 +75,23 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
     S[cc][r] = v;
   }
   __syncthreads();
-  // x_k = w_k * (1 / t_kk), like OpenBLAS' trsm kernels: one division per diagonal entry, all
-  // in parallel, instead of one (a ~150-cycle subroutine) per step on every column's chain —
-  // the non-unit kernel took 7x the unit one (config 2: 138 us per U table on the critical path)
+  // x_k = w_k / t_kk with the reciprocals computed once, all in parallel: q = w * r, then one
+  // residual correction q + r * fma(-t, q, w) — with r = RN(1 / t) that is the correctly rounded
+  // quotient (Markstein), i.e. the same bits as the IEEE division it replaces, but three dependent
+  // operations on every column's chain instead of a ~100-cycle division subroutine per step (the
+  // non-unit kernel took 7x the unit one; config 2: 138 us per U table on the critical path).
+  // The plain product w * r rounds differently and moved BASELINE config 4's near-threshold
+  // singular pivot from the reference's branch A/D/A/D to A/D/A.  Non-finite results (zero or
+  // non-finite diagonal) take the division itself.
   if (!UNIT) {
     if (threadIdx.x < T) rd[threadIdx.x] = 1.0 / S[threadIdx.x][threadIdx.x];
     __syncthreads();
   }
+  auto div_by = [](double w, double t, double r) {
+    const double q = w * r;
+    const double q1 = fma(fma(-t, q, w), r, q);
+    return (fabs(q1) <= 1.79769313486231570e308) ? q1 : w / t;   // NaN / Inf: the true division
+  };
   double x0[DINV_COLS], x1[DINV_COLS];   // column c = warp + DINV_WARPS * q: rows lane, lane + 32
 #pragma unroll
   for (int q = 0; q < DINV_COLS; ++q) {
@@ -96,8 +106,8 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
 #pragma unroll
       for (int q = 0; q < DINV_COLS; ++q) {
         if (!UNIT) {   // x_k *= 1 / l_kk before it propagates (forward substitution, non-unit)
-          const double rk = rd[k];
-          if (k >= 32) { if (lane == k - 32) x1[q] *= rk; } else { if (lane == k) x0[q] *= rk; }
+          const double rk = rd[k], dk = S[k][k];
+          if (k >= 32) { if (lane == k - 32) x1[q] = div_by(x1[q], dk, rk); } else { if (lane == k) x0[q] = div_by(x0[q], dk, rk); }
         }
         if (UNIT && k == T - 1) continue;
         const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
@@ -119,10 +129,10 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
   } else {
 #pragma unroll 2
     for (int k = T - 1; k >= 0; --k) {
-      const double rk = rd[k], s0 = S[k][lane], s1 = S[k][lane + 32];
+      const double rk = rd[k], dk = S[k][k], s0 = S[k][lane], s1 = S[k][lane + 32];
 #pragma unroll
       for (int q = 0; q < DINV_COLS; ++q) {
-        if (k >= 32) { if (lane == k - 32) x1[q] *= rk; } else { if (lane == k) x0[q] *= rk; }
+        if (k >= 32) { if (lane == k - 32) x1[q] = div_by(x1[q], dk, rk); } else { if (lane == k) x0[q] = div_by(x0[q], dk, rk); }
         const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0[q] : x1[q], k & 31);
         if (lane < k) x0[q] = fma(-s0, xk, x0[q]);
         if (lane + 32 < k) x1[q] = fma(-s1, xk, x1[q]);
