@@ -51,6 +51,8 @@ BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
 // independent substitution chains interleaved (shuffles, no block barriers on
 // the dependency chain).  Each column sees the same operation sequence as a
 // one-column-per-warp sweep.  dinv layout per item: [nblk][T x T column-major].
+__device__ __noinline__ double slow_div(double w, double t) { return w / t; }
+
 constexpr int DINV_WARPS = 8;
 constexpr int DINV_COLS = T / DINV_WARPS;   // columns per warp
 
@@ -89,8 +91,10 @@ __global__ void __launch_bounds__(DINV_WARPS * 32) dinv_kernel(ArenaView a, cons
   }
   auto div_by = [](double w, double t, double r) {
     const double q = w * r;
-    const double q1 = fma(fma(-t, q, w), r, q);
-    return (fabs(q1) <= 1.79769313486231570e308) ? q1 : w / t;   // NaN / Inf: the true division
+    double q1 = fma(fma(-t, q, w), r, q);
+    // NaN / Inf: the true division, out of line so that it is never speculated onto the chain
+    if (!(fabs(q1) <= 1.79769313486231570e308)) q1 = slow_div(w, t);
+    return q1;
   };
   double x0[DINV_COLS], x1[DINV_COLS];   // column c = warp + DINV_WARPS * q: rows lane, lane + 32
 #pragma unroll
