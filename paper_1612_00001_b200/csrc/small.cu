@@ -200,7 +200,11 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
         bi = pos[h];
       }
     }
+#if defined(BRI_SN_SKIP) && (BRI_SN_SKIP & 1)
+    bi = jn;               // experiment: no pivot search (timing only)
+#else
     warp_argmax_fast(bv, bi);
+#endif
     const int pp = (bi == INT_MAX) ? jn : bi;   // all NaN: pivot in place
     int oh = -1;
 #pragma unroll
@@ -215,7 +219,11 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     const double pv = __shfl_sync(0xffffffffu, mine, src);
     const int rp = __shfl_sync(0xffffffffu, lane + 32 * (oh < 0 ? 0 : oh), src);
     const bool recip = fabs(pv) >= kSfmin;
+#if defined(BRI_SN_SKIP) && (BRI_SN_SKIP & 2)
+    const double rinv = pv;   // experiment: no reciprocal (timing only)
+#else
     const double rinv = 1.0 / pv;
+#endif
 #pragma unroll
     for (int h = 0; h < R; ++h) {
       const int r = lane + 32 * h;
@@ -404,6 +412,9 @@ __global__ void __launch_bounds__(32 * sn_warps<N>(), 1) small_node_kernel(Arena
     // (dgetrs' L solve applies the same fma(-l_ij, w_j, w_i) in the same j order); register
     // columns left of qj are dead for every warp (compile-time), column qj is live only right
     // of j, and the lookahead column is already done
+#if defined(BRI_SN_SKIP) && (BRI_SN_SKIP & 4)
+    if (false)             // experiment: no trailing updates (timing only)
+#endif
 #pragma unroll
     for (int q = qj; q < Q; ++q) {
       const int c = warp + NW * q;
