@@ -5,8 +5,25 @@
 //   A: BM/16 boxes of 16 (m) x 16 (k) doubles, SWIZZLE_128B, 2 KB each
 //      (BRI_WIDE_A=0: BM/8 boxes of 8 x 16, SWIZZLE_64B — twice the TMA ops)
 //   B: one box of 16 (k) x BN (n) doubles, SWIZZLE_128B
-// The swizzles make the m16n8k4 fragment loads conflict-free (2 wavefronts
-// per 32 x 8 B request, the minimum).
+// Fragment loads and bank conflicts: a 64-bit shared load is served one HALF-WARP at a time
+// (16 lanes x 8 B = one 128-byte wavefront when the 16 addresses fall in 16 distinct 8-byte
+// bank pairs; ncu: 2 wavefronts per LDS.64 at best).  With the textbook m16n8k4 mapping
+// (fragment row g = lane / 4 <-> tile row g, fragment column g <-> tile column g) the 16 lanes
+// of a half-warp (g = 0..3 or 4..7, t = lane % 4 = 0..3) read from only 64 of the 128 bytes of
+// these swizzled rows, i.e. 4 wavefronts per load (profiles/r02_final_ncu_trsm_kernel_cfg3:
+// every swizzled LDS.64 at 4.0 wavefronts, "ideal" 2.0).  FragMap<true> therefore permutes
+// which tile row / column each fragment row / column stands for:
+//     fragment row  g + 8h (h = 0, 1)  <->  tile row  (s & 1) + 8 (s >> 1) + 2 q + 4 h
+//     fragment col  c                   <->  tile col  2 (c & 3) + (c >> 2)
+// with g = 4 q + s.  A half-warp then covers all 16 bank pairs in both operand layouts
+// (A: rows {0,1,8,9} + 2q + 4h under the XOR of k & 7 on 16-byte chunks; B: n & 7 = 2s + q
+// XORed onto the chunk index k / 2).  Every output element still accumulates its k range in
+// the same ascending k4 steps, so results are bit-identical to the textbook mapping; only the
+// owner thread of each C element changes, which the epilogues account for through
+// FragMap::row / FragMap::col.
+#ifndef BRI_FRAG_PERM
+#define BRI_FRAG_PERM 1
+#endif
 #pragma once
 
 #include "bri_common.cuh"
@@ -46,9 +63,20 @@ BRI_DEVI void tile_issue(uint8_t* st, uint64_t* full, const CUtensorMap* tmA, co
                 b_col + h * (BN / NBOX), b_slot);
 }
 
-// Warp-level accumulator of a (16*MI) x (8*NJ) sub-tile.
-template <int MI, int NJ>
+// Tile row (0..15) of fragment row g + 8h and tile column (0..7) of fragment column c.
+template <bool PERM>
+struct FragMap {
+  static BRI_DEVI int row(int g, int h) {
+    return PERM ? ((g & 1) + ((g & 2) << 2) + ((g & 4) >> 1) + (h << 2)) : (g + (h << 3));
+  }
+  static BRI_DEVI int col(int c) { return PERM ? (((c & 3) << 1) + (c >> 2)) : c; }
+};
+
+// Warp-level accumulator of a (16*MI) x (8*NJ) sub-tile.  c[i][j][v] is the element at tile row
+// 16 i + FragMap::row(lane / 4, v / 2), tile column 8 j + FragMap::col(2 (lane % 4) + (v & 1)).
+template <int MI, int NJ, bool PERM = (BRI_FRAG_PERM != 0)>
 struct WarpAcc {
+  using Map = FragMap<PERM>;
   double c[MI][NJ][4];
 
   BRI_DEVI void zero() {
@@ -73,7 +101,7 @@ struct WarpAcc {
       double a[MI][2], bf[NJ];
 #if BRI_WIDE_A
       const uint32_t sw = (k & 7) << 4;
-      const uint32_t off0 = k * 128 + ((g * 8) ^ sw), off1 = k * 128 + (((g + 8) * 8) ^ sw);
+      const uint32_t off0 = k * 128 + ((Map::row(g, 0) * 8) ^ sw), off1 = k * 128 + ((Map::row(g, 1) * 8) ^ sw);
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const uint8_t* box = sA + ((wm0 + i * 16) >> 4) * 2048;
@@ -81,6 +109,7 @@ struct WarpAcc {
         a[i][1] = kin ? *reinterpret_cast<const double*>(box + off1) : 0.0;
       }
 #else
+      static_assert(!PERM, "the permuted fragment map needs the 16-row A boxes");
       uint32_t offa = k * 64 + g * 8;
       offa ^= ((offa >> 7) & 3) << 4;
 #pragma unroll
@@ -92,7 +121,7 @@ struct WarpAcc {
 #endif
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        const int n = wn0 + j * 8 + g;
+        const int n = wn0 + j * 8 + Map::col(g);
         const uint32_t off = n * 128 + (((k >> 1) ^ (n & 7)) << 4) + ((k & 1) << 3);
         bf[j] = kin ? *reinterpret_cast<const double*>(sB + off) : 0.0;
       }
@@ -113,8 +142,8 @@ struct WarpAcc {
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          const int r = wm0 + i * 16 + g + ((v >> 1) << 3);
-          const int col = wn0 + j * 8 + 2 * t + (v & 1);
+          const int r = wm0 + i * 16 + Map::row(g, v >> 1);
+          const int col = wn0 + j * 8 + Map::col(2 * t + (v & 1));
           tile[col * ldt + r] = alpha * c[i][j][v];
         }
   }

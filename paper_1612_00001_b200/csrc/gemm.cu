@@ -35,6 +35,13 @@ namespace bri {
 
 namespace {
 
+#ifndef BRI_GEMM_PERM
+// Fragment map of the 128 x 128 GEMM (dmma_tile.cuh): the permuted, bank-conflict-free map halves its
+// LDS wavefronts, but the kernel is DMMA-bound (shared pipe 46% with the conflicts) and measured no
+// faster with it (b = 1024 level batch 9.60 vs 9.56 ms, config 3 925 vs 923 ms), so it keeps the textbook
+// map; the triangular-solve leaf, which is not, uses the permuted one.  Bits are identical either way.
+#define BRI_GEMM_PERM 0
+#endif
 #ifndef BRI_GEMM_STAGES
 #define BRI_GEMM_STAGES 4
 #endif
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int wm0 = (warp % WARPS_M) * WTM;
   const int wn0 = (warp / WARPS_M) * WTN;
-  WarpAcc<WTM / 16, WTN / 8> acc;
+  WarpAcc<WTM / 16, WTN / 8, (BRI_GEMM_PERM != 0)> acc;
   acc.zero();
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tm = rem % p.tiles_m;
     const int tn = rem / p.tiles_m;
     const int m0 = tm * BM, n0 = tn * BN;
-    WarpAcc<WTM / 16, WTN / 8> acc;
+    WarpAcc<WTM / 16, WTN / 8, (BRI_GEMM_PERM != 0)> acc;
     acc.zero();
     for (int kt = 0; kt < KT; ++kt) {
       const int gg = g0 + kt, s = gg % STAGES;
@@ -264,8 +271,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < JC; ++j)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            const int grow = m0 + wm0 + 16 * i + g + ((v >> 1) << 3);
-            const int gcol = n0 + wn0 + 8 * (j0 + j) + 2 * t + (v & 1);
+            const int grow = m0 + wm0 + 16 * i + decltype(acc)::Map::row(g, v >> 1);
+            const int gcol = n0 + wn0 + 8 * (j0 + j) + decltype(acc)::Map::col(2 * t + (v & 1));
             const bool ok = grow < p.M && gcol < p.N;
             old[j][v] = (ok && read_c) ? cin[(long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld] : 0.0;
           }
@@ -273,8 +280,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < JC; ++j)
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            const int grow = m0 + wm0 + 16 * i + g + ((v >> 1) << 3);
-            const int gcol = n0 + wn0 + 8 * (j0 + j) + 2 * t + (v & 1);
+            const int grow = m0 + wm0 + 16 * i + decltype(acc)::Map::row(g, v >> 1);
+            const int gcol = n0 + wn0 + 8 * (j0 + j) + decltype(acc)::Map::col(2 * t + (v & 1));
             if (grow < p.M && gcol < p.N) {
               const double val = p.alpha * acc.c[i][j0 + j][v];
               cout[(long long)(p.c_r0 + grow) + (long long)(p.c_c0 + gcol) * p.ld] =
@@ -332,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 // m16n8k4 steps from a zero accumulator, then fma(beta, C_in, alpha * acc))
 // is the big kernel's, so both paths give bit-identical results.
 constexpr int SK_BM = 64, SK_BN = 64, SK_KC = 32;
-constexpr int SK_LDA = SK_BM + 8;   // As[k][m]: A fragments 2 wavefronts
+constexpr int SK_LDA = SK_BM + 4;   // As[k][m]: 32 bytes mod 128 per k row, half-warp conflict-free (dmma_tile.cuh)
 constexpr int SK_LDB = SK_KC + 4;   // Bs[n][k]: B fragments 2 wavefronts
 
 __global__ void __launch_bounds__(256) skinny_kernel(GemmParams p) {

@@ -29,7 +29,11 @@ constexpr int T = TRSM_BLOCK;      // 64
 //   <16, 4>: a grid of <= one CTA per SM at 32 columns (a single factor's solve)
 //            is split twice as fine, again two CTAs per SM to hide the per-block-row latency.
 constexpr int THREADS = 256;
-constexpr int LDD = T + 8;         // Tinv tile stride (A-operand pattern: conflict-free)
+// Tile strides of the second product (textbook fragment map): a half-warp (4 values of
+// lane / 4 x 4 of lane % 4) must touch 16 distinct 8-byte bank pairs per 64-bit load, i.e. the
+// stride must be 32 bytes mod 128 in both operand patterns (T + 8 left the Tinv loads at 4
+// wavefronts per LDS.64 instead of 2).
+constexpr int LDD = T + 4;         // Tinv tile stride ([k][m], A-operand pattern)
 constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
 constexpr int LDB = T + 4;         // prefetched B_i tile stride ([n][k])
 template <int BN, int STAGES>
@@ -291,8 +295,9 @@ __global__ void __launch_bounds__(THREADS, 2)
     for (int j = 0; j < XJ; ++j)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int r = xm0 + g + ((v >> 1) << 3);
-        const int cc = xn0 + j * 8 + 2 * t + (v & 1);
+        // the accumulator's own (permuted) fragment map: see dmma_tile.cuh
+        const int r = xm0 + decltype(acc)::Map::row(g, v >> 1);
+        const int cc = xn0 + j * 8 + decltype(acc)::Map::col(2 * t + (v & 1));
         const bool ok = r < rows && c0 + cc < cend;
         R[cc * LDR + r] = ok ? Bst[cc * LDB + r] - acc.c[0][j][v] : 0.0;
       }
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 // update (capi.cu getrf_device): C = rt * U^-1, 128 columns per outer block.
 constexpr int RT_R = 32;               // rows per CTA
 constexpr int RT_THREADS = 128;        // 4 warps: 2 along M (16 rows) x 2 along N (32 cols)
-constexpr int RT_LDX = RT_R + 8;       // [col][row] tiles (A-operand pattern)
+constexpr int RT_LDX = RT_R + 4;       // [col][row] tiles (A-operand pattern: 32 bytes mod 128 per k row)
 constexpr int RT_LDU = T + 4;          // [n][k] tiles (B-operand pattern)
 constexpr int RT_SMEM = (3 * T * RT_LDX + T * RT_LDU) * 8;
 
