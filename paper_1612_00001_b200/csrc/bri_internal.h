@@ -91,8 +91,8 @@ struct GemmParams {
 int gemm_smem_bytes();
 int skinny_max_k();
 long long skinny_max_tiles();
-cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p,
-                        int count, cudaStream_t stream);
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB32,
+                        const GemmParams& p, int count, cudaStream_t stream);
 cudaError_t launch_scale_copy(const GemmParams& p, int count, cudaStream_t stream);
 
 // ---------------------------------------------------------------- LU pieces

@@ -241,7 +241,7 @@ int gemm_call(bri_arena* ar, cudaStream_t s, const int* dev_items, int count, in
   // tuning aid (BRI_GEMM_LOG=1): the shapes the solver issues, in capture order
   static const bool log_shapes = [] { const char* e = getenv("BRI_GEMM_LOG"); return e && *e == '1'; }();
   if (log_shapes) fprintf(stderr, "GEMMLOG %d %d %d %d %d\n", M, N, K, count, max_ctas);
-  BRI_CHECK(launch_gemm(ar->tmA, ar->tmB, p, count, s));
+  BRI_CHECK(launch_gemm(ar->tmA, ar->tmB, ar->tmB32, p, count, s));
   return 0;
 }
 

@@ -58,9 +58,31 @@ constexpr int TILE_BYTES = BN * LDT * 8;                 // 132 KB, reuses the s
 constexpr int RING_BYTES = STAGES * STAGE_BYTES > TILE_BYTES ? STAGES * STAGE_BYTES : TILE_BYTES;
 constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
-__global__ void __launch_bounds__(THREADS, 1)
+// Tile geometry of the one-tile-per-CTA kernel: 128 x BNT tiles, 4 x WNT warps of 32 x 32.
+//   <128, 4>: 512 threads, one CTA per SM (132 KB epilogue tile) — the long-K node GEMMs;
+//   < 64, 2>: 256 threads, TWO CTAs per SM (96 KB ring each): while one CTA streams its C tile
+//             (the epilogue is ~30% of a K = 128 tile and nothing hides it at one CTA per SM) the
+//             other one's DMMA loop owns the tensor pipe — the LU's rank-128 trailing updates.
+// Same per-element operation order in both (k ascending in k4 steps, then fma(beta, C_in, alpha * acc)).
+template <int BNT, int WNT>
+struct GemmGeom {
+  static constexpr int BN = BNT, WARPS_N = WNT, NUM_WARPS = WARPS_M * WNT, THREADS = NUM_WARPS * 32;
+  static constexpr int CTAS_PER_SM = BNT >= 128 ? 1 : 2;
+  static constexpr int NBOX = BNT >= 128 ? 1 : BNT / 32;   // narrow tiles load B through the 32-column map
+  static constexpr int STAGE_BYTES = StageGeom<BM, BNT>::BYTES;
+  static constexpr int TILE_BYTES = BNT * LDT * 8;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES > TILE_BYTES ? STAGES * STAGE_BYTES : TILE_BYTES;
+  static constexpr int SMEM_BYTES = RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BNT, int WNT>
+__global__ void __launch_bounds__((GemmGeom<BNT, WNT>::THREADS), (GemmGeom<BNT, WNT>::CTAS_PER_SM))
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 GemmParams p) {
+  using G = GemmGeom<BNT, WNT>;
+  constexpr int BN = G::BN, NUM_WARPS = G::NUM_WARPS, STAGE_BYTES = G::STAGE_BYTES, RING_BYTES = G::RING_BYTES;
+  constexpr int WTN = BN / G::WARPS_N;
+  static_assert(WTN == 32 && WTM == 32, "32 x 32 warp tiles");
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned (TMA 128B swizzle atoms) by pointer arithmetic on the
   // __shared__ array, so the compiler keeps the shared address space (LDS, not
@@ -93,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const bool producer = (warp == 0 && lane == 0);
   auto issue = [&](int kt) {
     const int s = kt % STAGES;
-    tile_issue<BM, BN>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, sa,
+    tile_issue<BM, BN, G::NBOX>(smem + s * STAGE_BYTES, &full[s], &tmA, &tmB, p.a_r0 + m0, p.a_c0 + kt * BK, sa,
                        p.b_r0 + kt * BK, p.b_c0 + n0, sb);
   };
   if (producer) {
@@ -440,14 +462,18 @@ long long skinny_max_tiles() {
 }
 
 cudaError_t configure_gemm() {
-  cudaError_t e = cudaFuncSetAttribute(gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  cudaError_t e = cudaFuncSetAttribute(gemm_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       GemmGeom<128, 4>::SMEM_BYTES);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             GemmGeom<64, 2>::SMEM_BYTES);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(gemm_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   return e;
 }
 
-cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmParams& p0,
-                        int count, cudaStream_t stream) {
+cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmB32,
+                        const GemmParams& p0, int count, cudaStream_t stream) {
   if (p0.M <= 0 || p0.N <= 0 || count <= 0) return cudaSuccess;
   GemmParams p = p0;
   p.tiles_m = (p.M + BM - 1) / BM;
@@ -499,7 +525,16 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     p.overlap = (cap_overlap && p.K <= cap_overlap) ? 1 : 0;
     gemm_persistent_kernel<<<dim3((unsigned)ctas), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
   } else {
-    gemm_kernel<<<dim3(p.tiles_m * p.tiles_n, count), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+    // BRI_GEMM_N64_MAXK: products with K at most this run on 128 x 64 tiles, two CTAs per SM
+    static const int n64_maxk = env_int("BRI_GEMM_N64_MAXK", 256);
+    if (p.K <= n64_maxk) {
+      using G = GemmGeom<64, 2>;
+      p.tiles_n = (p.N + G::BN - 1) / G::BN;
+      if ((long long)p.tiles_m * p.tiles_n > 0x7fffffffLL) return cudaErrorInvalidValue;
+      gemm_kernel<64, 2><<<dim3(p.tiles_m * p.tiles_n, count), G::THREADS, G::SMEM_BYTES, stream>>>(tmA, tmB32, p);
+    } else {
+      gemm_kernel<128, 4><<<dim3(p.tiles_m * p.tiles_n, count), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
+    }
   }
   return cudaGetLastError();
 }
