@@ -525,8 +525,13 @@ cudaError_t launch_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
     p.overlap = (cap_overlap && p.K <= cap_overlap) ? 1 : 0;
     gemm_persistent_kernel<<<dim3((unsigned)ctas), THREADS, SMEM_BYTES, stream>>>(tmA, tmB, p);
   } else {
-    // BRI_GEMM_N64_MAXK: products with K at most this run on 128 x 64 tiles, two CTAs per SM
-    static const int n64_maxk = env_int("BRI_GEMM_N64_MAXK", 256);
+    // 128 x 64 tiles, two CTAs per SM, for every K (BRI_GEMM_N64_MAXK=0 restores the 128 x 128
+    // tiles; = k: only products with K <= k).  Measured on 444-item b = 1024 batches, TFLOP/s
+    // 128x128 -> 128x64: K = 128 24.0 -> 28.4, K = 256 29.1 -> 32.4, K = 512 31.6 -> 33.5,
+    // K = 1024 33.3 -> 34.1; config 3 923 -> 886 ms; bit-identical results.  A 3-stage ring and
+    // the permuted fragment map were measured on it too: no gain (906.3 / 908.5 vs 906.5 ms at
+    // BRI_GEMM_N64_MAXK=256).
+    static const int n64_maxk = env_int("BRI_GEMM_N64_MAXK", 1 << 30);
     if (p.K <= n64_maxk) {
       using G = GemmGeom<64, 2>;
       p.tiles_n = (p.N + G::BN - 1) / G::BN;

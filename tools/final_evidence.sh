@@ -3,13 +3,14 @@
 # arm, configs 3 / 1 / 2), the ncu launch list of one config-3 step and `ncu --set full` captures of
 # the top kernels.  Each ncu pass runs only after the same command exited 0 without ncu.
 set -u
-OUT=gpurun_out/final
+OUT=${OUT:-gpurun_out/final}
 mkdir -p $OUT
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf --durations=12 > $OUT/gputest.log 2>&1; echo "rc=$?" >> $OUT/gputest.log
 timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench_cfg3.json 2> $OUT/bench_cfg3.err; echo "rc=$?" >> $OUT/bench_cfg3.err
 ( time timeout 1500 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/ref_cfg3.json ) 2> $OUT/ref_cfg3.err
 timeout 600 python bench.py --config 1 --steps 20 --warmup 5 > $OUT/bench_cfg1.json 2> $OUT/bench_cfg1.err
 timeout 600 python bench.py --config 2 --steps 20 --warmup 5 > $OUT/bench_cfg2.json 2> $OUT/bench_cfg2.err
+for c in 1 2 3; do timeout 600 python tools/hash_config.py --config $c >> $OUT/hashes.txt 2>> $OUT/hashes.err; done
 timeout 600 python tools/timeline.py --config 3 --out $OUT/timeline_cfg3.json > $OUT/timeline_cfg3.txt 2>&1
 timeout 600 python tools/timeline.py --config 2 --out $OUT/timeline_cfg2.json > $OUT/timeline_cfg2.txt 2>&1
 python tools/chain_gaps.py $OUT/timeline_cfg2.json > $OUT/chain_cfg2.txt 2>&1
