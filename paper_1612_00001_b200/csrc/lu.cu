@@ -196,8 +196,11 @@ BRI_DEVI void store_u_row(double* psm, int rhp, int jj, int nb, int slot, const 
     if (jj + c < nb) psm[(jj + c) * rhp + slot] = xr[c];
 }
 
-template <int RPT>
-__global__ void __launch_bounds__(PT, 1) lu_panel_kernel(PanelArgs p) {
+// MINB = 2 (one row per thread only): capped at 128 registers (~100 bytes of spills) so that two
+// CTAs share an SM — large batches run the panels in many waves, and two resident column chains per
+// SM hide each other's latency (launch_panel).
+template <int RPT, int MINB = 1>
+__global__ void __launch_bounds__(PT, MINB) lu_panel_kernel(PanelArgs p) {
   if (p.early) pdl_trigger();
   pdl_wait();   // launched programmatically after the previous chain kernel
   constexpr int SW = 34;
@@ -823,7 +826,7 @@ cudaError_t launch_pi_init(int* pi, int n, int count, unsigned long long* scale_
 // Panel width: 32 columns, held in registers (up to 2 rows x 32 per thread).
 int panel_width(int n) { return n > 0 ? NBMAX : NBMAX; }
 
-template <int RPT>
+template <int RPT, int MINB = 1>
 static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s) {
   const size_t smem = (size_t)p.nb * p.rhp * 8 + (size_t)p.rhp * 4 + 16;
   if (smem > 160 * 1024) return cudaErrorInvalidValue;
@@ -841,13 +844,15 @@ static cudaError_t launch_panel_t(PanelArgs p, int cs, int count, cudaStream_t s
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   count_launch();
-  return cudaLaunchKernelEx(&cfg, lu_panel_kernel<RPT>, p);
+  return cudaLaunchKernelEx(&cfg, lu_panel_kernel<RPT, MINB>, p);
 }
 
 cudaError_t configure_lu() {
   cudaError_t e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lu_panel_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(lu_panel_tall_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -897,10 +902,19 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
     const char* e = getenv("BRI_PANEL_RPT2_WAVES");
     return e ? atoi(e) : 2;
   }();
+  // BRI_PANEL_2CTA=1: instead, keep one row per thread and run two CTAs per SM (128 registers)
+  static const int two_cta = [] {
+    const char* e = getenv("BRI_PANEL_2CTA");
+    return e ? atoi(e) : 0;
+  }();
   int rpt = h <= PORTABLE_CS * PT ? 1 : 2;
+  bool dense = false;
   if (rpt == 1 && h > PT) {
     const long long ctas1 = (long long)count * ((h + PT - 1) / PT);
-    if (ctas1 > (long long)wide_waves * 148) rpt = 2;
+    if (ctas1 > (long long)wide_waves * 148) {
+      if (two_cta) dense = true;
+      else rpt = 2;
+    }
   }
   int cs = 1;
   while (cs < MAXCS && (h + cs - 1) / cs > rpt * PT) cs <<= 1;
@@ -918,6 +932,7 @@ cudaError_t launch_panel(const ArenaView& a, const int* slots, int count, int j0
   p.n_stride = n_stride;
   p.pair_stride = pair_stride;
   p.early = early ? 1 : 0;
+  if (dense && (size_t)p.nb * p.rhp * 8 + (size_t)p.rhp * 4 + 16 <= 100 * 1024) return launch_panel_t<1, 2>(p, cs, count, s);
   if (rpt == 1) return launch_panel_t<1>(p, cs, count, s);
   return launch_panel_t<2>(p, cs, count, s);
 }
