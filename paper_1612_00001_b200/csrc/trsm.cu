@@ -36,9 +36,17 @@ constexpr int THREADS = 256;
 constexpr int LDD = T + 4;         // Tinv tile stride ([k][m], A-operand pattern)
 constexpr int LDR = T + 4;         // R tile stride ([n][k], B-operand pattern)
 constexpr int LDB = T + 4;         // prefetched B_i tile stride ([n][k])
-template <int BN, int STAGES>
+// DENSE: three CTAs per SM (<= 76,800 bytes each): the Tinv tile unpadded with an XOR swizzle on
+// 32-byte groups (same half-warp property as the padded stride), the prefetched B_i tile shares the R
+// buffer (R = B_i - acc is computed in place by the thread that owns each element) and the ring has
+// two stages.
+template <int BN, int STAGES, bool DENSE = false>
 constexpr int smem_bytes() {
-  return STAGES * StageGeom<T, BN>::BYTES + T * LDD * 8 + 2 * BN * LDR * 8 + 1024 + 256;
+  return STAGES * StageGeom<T, BN>::BYTES + T * (DENSE ? T : LDD) * 8 + (DENSE ? 1 : 2) * BN * LDR * 8 + 1024 + 256;
+}
+template <bool DENSE>
+BRI_DEVI int tinv_index(int k, int m) {
+  return DENSE ? k * T + (m ^ ((k & 3) << 2)) : k * LDD + m;
 }
 
 BRI_DEVI void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
@@ -170,8 +178,8 @@ struct TrsmArgs {
                         // being inverted): rows above a column's diagonal are zero and stay zero
 };
 
-template <bool LOWER, int BN, int STAGES>
-__global__ void __launch_bounds__(THREADS, 2)
+template <bool LOWER, int BN, int STAGES, bool DENSE = false>
+__global__ void __launch_bounds__(THREADS, (DENSE ? 3 : 2))
     trsm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TrsmArgs p) {
   constexpr int SB = StageGeom<T, BN>::BYTES;
   constexpr int XJ = BN / 16;       // n8 tiles per warp (4 warps along M x 2 along N, 16 x BN/2 each)
@@ -182,8 +190,8 @@ __global__ void __launch_bounds__(THREADS, 2)
   // generic LD with 64-bit address math) for every fragment load
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   double* D = reinterpret_cast<double*>(smem + STAGES * SB);   // Tinv_ii, [k][m] col-major (LDD)
-  double* R = D + T * LDD;                                              // B_i - acc, [n][k] (LDR)
-  double* Bst = R + BN * LDR;                                           // prefetched B_i, [n][k] (LDB)
+  double* R = D + T * (DENSE ? T : LDD);                                // B_i - acc, [n][k] (LDR)
+  double* Bst = DENSE ? R : R + BN * LDR;                               // prefetched B_i, [n][k] (LDB)
   uint64_t* full = reinterpret_cast<uint64_t*>(Bst + BN * LDB);
   uint64_t* empty = full + STAGES;
 
@@ -240,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 2)
       const double* Di = dinv + (long long)(row0 / T) * T * T;
       for (int e = threadIdx.x; e < T * T / 2; e += THREADS) {
         const int k = e / (T / 2), r2 = (e % (T / 2)) * 2;
-        cp_async16(&D[k * LDD + r2], Di + k * T + r2, true);
+        cp_async16(&D[tinv_index<DENSE>(k, r2)], Di + k * T + r2, true);
       }
       for (int e = threadIdx.x; e < BN * T / 2; e += THREADS) {
         const int cc = e / (T / 2), r2 = (e % (T / 2)) * 2;
@@ -310,8 +318,8 @@ __global__ void __launch_bounds__(THREADS, 2)
       for (int v = 0; v < 4; ++v) x[j][v] = 0.0;
 #pragma unroll 4
     for (int k0 = 0; k0 < T; k0 += 4) {
-      const double a0 = D[(k0 + t) * LDD + xm0 + g];
-      const double a1 = D[(k0 + t) * LDD + xm0 + g + 8];
+      const double a0 = D[tinv_index<DENSE>(k0 + t, xm0 + g)];
+      const double a1 = D[tinv_index<DENSE>(k0 + t, xm0 + g + 8)];
 #pragma unroll
       for (int j = 0; j < XJ; ++j) {
         const double b0 = R[(xn0 + j * 8 + g) * LDR + k0 + t];
@@ -448,6 +456,8 @@ cudaError_t configure_trsm() {
   set((const void*)trsm_kernel<false, 64, 4>, smem_bytes<64, 4>());
   set((const void*)trsm_kernel<true, 16, 4>, smem_bytes<16, 4>());
   set((const void*)trsm_kernel<false, 16, 4>, smem_bytes<16, 4>());
+  set((const void*)trsm_kernel<true, 32, 2, true>, smem_bytes<32, 2, true>());
+  set((const void*)trsm_kernel<false, 32, 2, true>, smem_bytes<32, 2, true>());
   set((const void*)rtrsm_kernel, RT_SMEM);
   return e;
 }
@@ -524,6 +534,11 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
     const char* e = getenv("BRI_TRSM_BN64");
     return e != nullptr ? atoi(e) : 0;
   }();
+  // BRI_TRSM_DENSE=1: large batches on the three-CTA-per-SM variant
+  static const int dense_env = [] {
+    const char* e = getenv("BRI_TRSM_DENSE");
+    return e != nullptr ? atoi(e) : 0;
+  }();
   // nr x nr triangle against nrhs columns (tri_rhs: column c starts at its diagonal)
   double per = (double)nr * nr * nrhs;
   if (tri_rhs) {
@@ -549,6 +564,10 @@ cudaError_t launch_trsm_fused(const CUtensorMap& tmA, const CUtensorMap& tmB32, 
     dim3 grid((nrhs + 63) / 64, count);
     if (lower) trsm_kernel<true, 64, 4><<<grid, THREADS, smem_bytes<64, 4>(), s>>>(tmA, tmB32, p);
     else trsm_kernel<false, 64, 4><<<grid, THREADS, smem_bytes<64, 4>(), s>>>(tmA, tmB32, p);
+  } else if (dense_env) {
+    dim3 grid((nrhs + 31) / 32, count);
+    if (lower) trsm_kernel<true, 32, 2, true><<<grid, THREADS, smem_bytes<32, 2, true>(), s>>>(tmA, tmB32, p);
+    else trsm_kernel<false, 32, 2, true><<<grid, THREADS, smem_bytes<32, 2, true>(), s>>>(tmA, tmB32, p);
   } else {
     dim3 grid((nrhs + 31) / 32, count);
     if (lower) trsm_kernel<true, 32, 3><<<grid, THREADS, smem_bytes<32, 3>(), s>>>(tmA, tmB32, p);
